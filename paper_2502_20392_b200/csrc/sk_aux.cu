@@ -1,0 +1,254 @@
+// Auxiliary kernels around the sweep: increments (K1), the order pre-pass
+// (per-series increment norms for the Cauchy-Schwarz bound and the exact
+// max|rho| scan), the skewed rho table for large d, knot-grid boundary
+// initialisation and single-tile entry points.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sk_device.cuh"
+#include "sk_internal.h"
+
+namespace skb {
+
+// time_series.cpp:32-42: dz_k = z_{k+1} - z_k, (len-1) x dim row-major per series.
+__global__ void increments_kernel(const double* __restrict__ v, size_t nseries, size_t len, size_t dim,
+                                  double* __restrict__ out) {
+  const size_t per = (len - 1) * dim;
+  const size_t total = nseries * per;
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t s = t / per;
+    const size_t k = t - s * per;
+    const double* src = v + s * len * dim + k;
+    out[t] = src[dim] - src[0];
+  }
+}
+
+// Per series: max_k sum_c dz_k[c]^2 (only feeds the Cauchy-Schwarz upper
+// bound of max|rho|, so its rounding is covered by the bound's slack).
+__global__ void max_sqnorm_kernel(const double* __restrict__ inc, size_t count, size_t dim,
+                                  double* __restrict__ out) {
+  const double* s = inc + blockIdx.x * count * dim;
+  double best = 0.0;
+  for (size_t k = threadIdx.x; k < count; k += blockDim.x) {
+    double acc = 0.0;
+    for (size_t c = 0; c < dim; ++c) acc = fma(s[k * dim + c], s[k * dim + c], acc);
+    best = fmax(best, acc);
+  }
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (threadIdx.x == 0) out[blockIdx.x] = best;
+  }
+}
+
+// Exact max|rho| per pair (time_series.cpp:64-73): sequential non-FMA dot in
+// coordinate order, so the value is bit-identical and estimate_order's
+// thresholds cannot flip.  blockIdx.y = launch-local pair; threads own rows.
+template <int DP>
+__global__ void maxrho_scan_kernel(const double* __restrict__ xinc, const double* __restrict__ yinc,
+                                   const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                                   unsigned long long sx, unsigned long long sy, int rows, int cols, int dim,
+                                   unsigned long long* __restrict__ out) {
+  const int pr = blockIdx.y;
+  const double* xs = xinc + px[pr] * sx;
+  const double* ys = yinc + py[pr] * sy;
+  double best = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    const double* yr = ys + static_cast<size_t>(i) * dim;
+    if constexpr (DP > 0) {
+      double yv[DP];
+#pragma unroll
+      for (int c = 0; c < DP; ++c) yv[c] = (c < dim) ? yr[c] : 0.0;
+      for (int j = 0; j < cols; ++j) {
+        const double* xr = xs + static_cast<size_t>(j) * dim;
+        double xv[DP];
+#pragma unroll
+        for (int c = 0; c < DP; ++c) xv[c] = (c < dim) ? __ldg(xr + c) : 0.0;
+        const double a = fabs(exact_dot<DP>(xv, yv));
+        if (best < a) best = a;
+      }
+    } else {
+      for (int j = 0; j < cols; ++j) {
+        const double* xr = xs + static_cast<size_t>(j) * dim;
+        double acc = __dmul_rn(__ldg(xr), yr[0]);
+        for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + c), yr[c]));
+        const double a = fabs(acc);
+        if (best < a) best = a;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best > 0.0)
+    atomicMax(out + pr, static_cast<unsigned long long>(__double_as_longlong(best)));
+}
+
+// Skewed delta table for the large-d path: entry ((b*(cols+31) + s)*32 + t)
+// holds rho(i = 32b + t, j = s - t) (0 outside the pair), so the sweep's warp
+// reads 256 contiguous bytes per step.  Exact sequential dot.
+__global__ void rho_table_kernel(const double* __restrict__ xinc, const double* __restrict__ yinc,
+                                 const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                                 unsigned long long sx, unsigned long long sy, int rows, int cols, int bands,
+                                 int dim, double* __restrict__ tab, unsigned long long tab_stride) {
+  const int pr = blockIdx.y;
+  const double* xs = xinc + px[pr] * sx;
+  const double* ys = yinc + py[pr] * sy;
+  double* t = tab + pr * tab_stride;
+  const size_t steps = static_cast<size_t>(cols) + 31;
+  const size_t total = static_cast<size_t>(bands) * steps * 32;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int lane = static_cast<int>(e & 31);
+    const size_t bs = e >> 5;
+    const int b = static_cast<int>(bs / steps);
+    const int s = static_cast<int>(bs - static_cast<size_t>(b) * steps);
+    const int i = b * 32 + lane;
+    const int j = s - lane;
+    double v = 0.0;
+    if (i < rows && j >= 0 && j < cols) {
+      const double* xr = xs + static_cast<size_t>(j) * dim;
+      const double* yr = ys + static_cast<size_t>(i) * dim;
+      double acc = __dmul_rn(__ldg(xr), __ldg(yr));
+      for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + c), __ldg(yr + c)));
+      v = acc;
+    }
+    t[e] = v;
+  }
+}
+
+// Knot grid boundary (wavefront.cpp:92-98): K = 1 on a = 0 and b = 0.
+__global__ void grid_init_kernel(double* grid, size_t nout, size_t lx, size_t ly) {
+  const size_t per = lx * ly;
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < nout * per;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t e = t % per;
+    const size_t a = e / ly, b = e - a * ly;
+    if (a == 0 || b == 0) grid[t] = 1.0;
+  }
+}
+
+// step_tile with the reference's exact arithmetic (one thread).
+// io: in = alpha[65] | beta[65]; out = alpha'[65] | beta'[65] | total
+__global__ void step_tile_literal_kernel(double delta, int order, const double* __restrict__ w65,
+                                         const double* __restrict__ in, double* __restrict__ out) {
+  double a[kMaxOrder + 1], b[kMaxOrder + 1], oa[kMaxOrder + 1], ob[kMaxOrder + 1];
+  for (int m = 0; m <= order; ++m) {
+    a[m] = in[m];
+    b[m] = in[kMaxOrder + 1 + m];
+  }
+  const double total = tile_step_literal(order, a, b, delta, w65, oa, ob);
+  for (int m = 0; m <= order; ++m) {
+    out[m] = oa[m];
+    out[kMaxOrder + 1 + m] = ob[m];
+  }
+  out[2 * (kMaxOrder + 1)] = total;
+}
+
+template <int N>
+__global__ void step_tile_fast_kernel(double delta, const double* __restrict__ in, double* __restrict__ out) {
+  double q[N + 1], r[N + 1], qo[N + 1], ro[N + 1];
+  double f = 1.0;
+#pragma unroll
+  for (int m = 0; m <= N; ++m) {
+    if (m > 0) f *= m;
+    q[m] = in[m] * f;
+    r[m] = in[kMaxOrder + 1 + m] * f;
+  }
+  const double total = tile_step_scaled<N>(q, r, delta, qo, ro, false);
+#pragma unroll
+  for (int m = 0; m <= N; ++m) {
+    out[m] = qo[m] * c_inv_fact[m];
+    out[kMaxOrder + 1 + m] = ro[m] * c_inv_fact[m];
+  }
+  out[2 * (kMaxOrder + 1)] = total;
+}
+
+// ------------------------------------------------------------- launchers
+static int grid_for(size_t work, int threads) {
+  size_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return static_cast<int>(g);
+}
+
+cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, double* out,
+                              cudaStream_t st) {
+  const size_t work = nseries * (len - 1) * dim;
+  if (work == 0) return cudaSuccess;
+  increments_kernel<<<grid_for(work, 256), 256, 0, st>>>(v, nseries, len, dim, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, double* out,
+                              cudaStream_t st) {
+  if (nseries == 0) return cudaSuccess;
+  max_sqnorm_kernel<<<static_cast<unsigned>(nseries), 256, 0, st>>>(inc, count, dim, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
+                               size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
+                               int dim, unsigned long long* out, cudaStream_t st) {
+  if (npairs == 0) return cudaSuccess;
+  const int threads = 128;
+  const int bx = (rows + threads - 1) / threads;
+  const dim3 grid(bx, static_cast<unsigned>(npairs));
+  const int dp = pick_dp(dim);
+  switch (dp) {
+    case 2: maxrho_scan_kernel<2><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
+    case 4: maxrho_scan_kernel<4><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
+    case 8: maxrho_scan_kernel<8><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
+    case 16: maxrho_scan_kernel<16><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
+    default: maxrho_scan_kernel<0><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
+                             size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
+                             int bands, int dim, double* tab, unsigned long long tab_stride, cudaStream_t st) {
+  if (npairs == 0) return cudaSuccess;
+  const size_t per = static_cast<size_t>(bands) * (cols + 31) * 32;
+  const int threads = 256;
+  size_t bx = (per + threads - 1) / threads;
+  if (bx > 4096) bx = 4096;
+  const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(npairs));
+  rho_table_kernel<<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, bands, dim, tab, tab_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grid_init(double* grid, size_t nout, size_t lx, size_t ly, cudaStream_t st) {
+  const size_t work = nout * lx * ly;
+  if (work == 0) return cudaSuccess;
+  grid_init_kernel<<<grid_for(work, 256), 256, 0, st>>>(grid, nout, lx, ly);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_tile_literal(double delta, int order, const double* w65, const double* in, double* out,
+                                     cudaStream_t st) {
+  step_tile_literal_kernel<<<1, 1, 0, st>>>(delta, order, w65, in, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_tile_fast(double delta, int order, const double* in, double* out, cudaStream_t st) {
+  switch (order) {
+#define SK_FAST_CASE(NN) \
+  case NN: step_tile_fast_kernel<NN><<<1, 1, 0, st>>>(delta, in, out); break;
+    SK_FAST_CASE(1) SK_FAST_CASE(2) SK_FAST_CASE(3) SK_FAST_CASE(4) SK_FAST_CASE(5) SK_FAST_CASE(6)
+    SK_FAST_CASE(7) SK_FAST_CASE(8) SK_FAST_CASE(9) SK_FAST_CASE(10) SK_FAST_CASE(11) SK_FAST_CASE(12)
+    SK_FAST_CASE(13) SK_FAST_CASE(14) SK_FAST_CASE(15) SK_FAST_CASE(16)
+#undef SK_FAST_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace skb

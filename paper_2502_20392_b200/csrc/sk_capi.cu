@@ -1,0 +1,939 @@
+// The C-ABI (include/sigker_b200.h): host orchestration of the B200 path.
+//
+// Per call: H2D of the series -> increments kernel (K1) -> order pre-pass
+// (Cauchy-Schwarz bound, exact max|rho| scan only where the bound cannot
+// prove the order) -> one persistent banded sweep launch per distinct order
+// (K2 + K3 fused) -> D2H of values / error keys / max|rho|.
+// Per host thread: one context = device, stream, grow-only workspace.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "sigker_b200.h"
+#include "sk_internal.h"
+#include "sk_sweep.cuh"
+
+namespace {
+
+using namespace skb;
+
+// ------------------------------------------------------------------ status
+int set_status(sk_status* st, int code, uint64_t k, uint64_t l, const char* fmt, ...) {
+  if (st) {
+    st->code = code;
+    st->tile_k = k;
+    st->tile_l = l;
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(st->message, sizeof st->message, fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+void clear_status(sk_status* st) {
+  if (st) std::memset(st, 0, sizeof *st);
+}
+
+int cuda_fail(sk_status* st, cudaError_t e, const char* where) {
+  return set_status(st, SK_CUDA_ERROR, 0, 0, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define SK_CUDA(call)                                       \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return cuda_fail(st, e_, #call); \
+  } while (0)
+
+// ------------------------------------------------------------ host tables
+const double* host_factorials() {
+  static double fact[171];
+  static bool ready = false;
+  if (!ready) {
+    fact[0] = 1.0;
+    for (int k = 1; k < 171; ++k) fact[k] = fact[k - 1] * static_cast<double>(k);  // tile_series.cpp:19-27
+    ready = true;
+  }
+  return fact;
+}
+
+// truncation.cpp:41-55 at unit boundaries (tile_series.cpp:123-132 entry
+// expression c = B * (A * W)); identical floating-point operations.
+int host_estimate_order(double rho, double tol, int* order, int* converged) {
+  const double* fact = host_factorials();
+  for (int n = 8; n <= kMaxOrder; ++n) {
+    double pw[kMaxOrder + 1];
+    pw[0] = 1.0;
+    for (int m = 1; m <= n; ++m) pw[m] = pw[m - 1] * rho;
+    double tail = 0.0;
+    for (int j = 0; j <= n; ++j) {
+      const double b = (j == n) ? 1.0 : 0.0;
+      const int lo = j < n ? j : n, hi = j < n ? n : j;
+      tail += b * (pw[lo] * (fact[hi - lo] / (fact[hi] * fact[lo])));
+    }
+    for (int i = 0; i <= n; ++i) {
+      const double b = (i == n) ? 1.0 : 0.0;
+      const int lo = i < n ? i : n, hi = i < n ? n : i;
+      tail += b * (pw[lo] * (fact[hi - lo] / (fact[hi] * fact[lo])));
+    }
+    if (tail < tol) {
+      *order = n;
+      *converged = 1;
+      return SK_OK;
+    }
+  }
+  *order = kMaxOrder;
+  *converged = 0;
+  return SK_OK;
+}
+
+// wavefront.cpp:19-30,107,111-125,175-176 -- the 1-thread live-series
+// counter in closed form: the count only rises in prefill_units, and inside a
+// diagonal every tile does sub(2) then add(up + right <= 2), so the peak is
+// reached right after a prefill.  O(rows + cols).
+uint64_t peak_live_closed_form(uint64_t rows, uint64_t cols) {
+  int64_t cur = 2, peak = 2;  // prefill_units(0): both edges live
+  const uint64_t diagonals = rows + cols - 1;
+  for (uint64_t d = 0; d < diagonals; ++d) {
+    if (d + 1 < diagonals) {
+      cur += (d + 1 <= cols - 1 ? 1 : 0) + (d + 1 <= rows - 1 ? 1 : 0);
+      if (cur > peak) peak = cur;
+    }
+    cur -= (d >= rows - 1 ? 1 : 0) + (d >= cols - 1 ? 1 : 0);
+  }
+  return static_cast<uint64_t>(peak);
+}
+
+// ----------------------------------------------------------------- context
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+      cap = 0;
+    }
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return e;
+    }
+    cap = want;
+    return cudaSuccess;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct StatRec {
+  cudaEvent_t a, b;
+  double tiles, flops;
+};
+
+struct Ctx {
+  int device = 0;
+  bool ready = false;
+  cudaStream_t own = nullptr;
+  cudaStream_t user = nullptr;
+  int sms = 148;
+  DevBuf raw_x, raw_y, xinc, yinc, sqn, pairs, values, err, maxr, prog, queue, abuf, tab, grid, diag, w65, tile_io,
+      scan;
+  bool stats_on = false;
+  std::vector<StatRec> stats;
+  uint64_t sweep_launches = 0, aux_launches = 0;
+  double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0;
+
+  cudaStream_t stream() const { return user ? user : own; }
+  ~Ctx() {
+    for (auto& r : stats) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    DevBuf* all[] = {&raw_x, &raw_y, &xinc, &yinc, &sqn, &pairs, &values, &err, &maxr,
+                     &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan};
+    for (DevBuf* b : all) b->release();
+    if (own) cudaStreamDestroy(own);
+  }
+};
+
+thread_local std::unique_ptr<Ctx> t_ctx;
+thread_local int t_device = 0;
+
+int get_ctx(Ctx** out, sk_status* st) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return set_status(st, SK_CUDA_ERROR, 0, 0,
+                      "no CUDA device available (the B200 path has no CPU fallback): %s",
+                      e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  }
+  if (t_ctx && t_ctx->device != t_device) t_ctx.reset();
+  if (!t_ctx) {
+    auto c = std::make_unique<Ctx>();
+    c->device = t_device;
+    SK_CUDA(cudaSetDevice(c->device));
+    SK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    SK_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+    // W table, row stride 65 (tile_series.cpp:41-53 build_W_into)
+    const double* fact = host_factorials();
+    std::vector<double> w((kMaxOrder + 1) * (kMaxOrder + 1));
+    for (int i = 0; i <= kMaxOrder; ++i)
+      for (int j = i; j <= kMaxOrder; ++j) {
+        const double v = fact[j - i] / (fact[j] * fact[i]);
+        w[i * (kMaxOrder + 1) + j] = v;
+        w[j * (kMaxOrder + 1) + i] = v;
+      }
+    SK_CUDA(c->w65.ensure(w.size() * sizeof(double)));
+    SK_CUDA(cudaMemcpy(c->w65.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    c->ready = true;
+    t_ctx = std::move(c);
+  }
+  SK_CUDA(cudaSetDevice(t_ctx->device));
+  *out = t_ctx.get();
+  return SK_OK;
+}
+
+// --------------------------------------------------------------- sweeps
+struct PairSet {
+  const double* d_xinc;
+  const double* d_yinc;
+  unsigned long long sx, sy;  // elements between series
+  int rows, cols, dim;
+};
+
+struct Outputs {
+  double* d_values;              // indexed by output slot
+  unsigned long long* d_err;     // indexed by output slot
+  unsigned long long* d_maxrho;  // may be null
+  double* d_grid;                // may be null
+  double* d_diag;                // may be null
+  unsigned long long grid_stride, diag_stride;
+};
+
+double flops_per_tile(int order, int dim) {
+  const double n = order + 1;
+  return 4.0 * n * n + 2.0 * dim;  // F(N, d)
+}
+
+int record_start(Ctx& c, StatRec* rec, sk_status* st) {
+  if (!c.stats_on) return SK_OK;
+  SK_CUDA(cudaEventCreate(&rec->a));
+  SK_CUDA(cudaEventCreate(&rec->b));
+  SK_CUDA(cudaEventRecord(rec->a, c.stream()));
+  return SK_OK;
+}
+
+int record_end(Ctx& c, StatRec* rec, sk_status* st) {
+  if (!c.stats_on) return SK_OK;
+  SK_CUDA(cudaEventRecord(rec->b, c.stream()));
+  c.stats.push_back(*rec);
+  return SK_OK;
+}
+
+// One persistent sweep launch per (order, pair chunk).  px/py/pout are
+// launch-local pair lists of equal length.
+int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const std::vector<uint32_t>& py,
+               const std::vector<uint32_t>& pout, int order, uint32_t flags, const Outputs& o, sk_status* st) {
+  const size_t npairs_all = px.size();
+  if (npairs_all == 0) return SK_OK;
+  const int ntempl = order <= kMaxRegOrder ? order : 0;
+  const int dp = pick_dp(ps.dim);
+  const int na = ntempl > 0 ? ntempl + 1 : kMaxOrder + 1;
+  const int np = (na + 1) & ~1;
+  const int rows = ps.rows, cols = ps.cols;
+  const int bands = (rows + 31) / 32;
+  int bps = 0;
+  SK_CUDA(sweep_occupancy(ntempl, dp, &bps));
+  if (bps < 1) return set_status(st, SK_CUDA_ERROR, 0, 0, "sweep kernel cannot be resident (occupancy 0)");
+  size_t free_b = 0, total_b = 0;
+  SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+
+  // large d: per-pair skewed rho tables, pairs chunked to a memory budget
+  const size_t tab_elems = dp == 0 ? static_cast<size_t>(bands) * (cols + 31) * 32 : 0;
+  size_t chunk = npairs_all;
+  if (dp == 0) {
+    const size_t budget = std::max<size_t>(free_b / 3, tab_elems * sizeof(double));
+    chunk = std::max<size_t>(1, budget / (tab_elems * sizeof(double)));
+  }
+  // units per launch must fit 32 bits
+  chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / bands));
+
+  for (size_t c0 = 0; c0 < npairs_all; c0 += chunk) {
+    const size_t npairs = std::min(chunk, npairs_all - c0);
+    const unsigned long long units = static_cast<unsigned long long>(npairs) * bands;
+    int blocks = bps * c.sms;
+    const unsigned long long need_blocks = (units + kSweepWarps - 1) / kSweepWarps;
+    if (static_cast<unsigned long long>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
+    const size_t warps = static_cast<size_t>(blocks) * kSweepWarps;
+    size_t group = npairs >= warps ? warps : npairs;
+    size_t slots = std::min(npairs, 2 * group);
+    const size_t col_bytes = static_cast<size_t>(cols) * np * sizeof(double);
+    if (bands > 1) {
+      const size_t budget = std::max<size_t>(free_b / 4, col_bytes);
+      const size_t fit = std::max<size_t>(1, budget / col_bytes);
+      if (slots > fit) slots = std::max<size_t>(fit, 1);
+      if (group > slots) group = slots;
+    }
+    // workspace
+    SK_CUDA(c.pairs.ensure(3 * npairs * sizeof(uint32_t)));
+    uint32_t* d_px = c.pairs.as<uint32_t>();
+    uint32_t* d_py = d_px + npairs;
+    uint32_t* d_po = d_py + npairs;
+    SK_CUDA(cudaMemcpyAsync(d_px, px.data() + c0, npairs * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
+    SK_CUDA(cudaMemcpyAsync(d_py, py.data() + c0, npairs * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
+    SK_CUDA(cudaMemcpyAsync(d_po, pout.data() + c0, npairs * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
+    SK_CUDA(c.prog.ensure(slots * bands * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemsetAsync(c.prog.p, 0, slots * bands * sizeof(unsigned long long), c.stream()));
+    SK_CUDA(c.queue.ensure(sizeof(unsigned)));
+    SK_CUDA(cudaMemsetAsync(c.queue.p, 0, sizeof(unsigned), c.stream()));
+    if (bands > 1) SK_CUDA(c.abuf.ensure(slots * col_bytes));
+    if (dp == 0) {
+      SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
+      SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, bands, ps.dim,
+                               c.tab.as<double>(), tab_elems, c.stream()));
+      ++c.aux_launches;
+    }
+    SweepParams P{};
+    P.xinc = ps.d_xinc;
+    P.yinc = ps.d_yinc;
+    P.pair_x = d_px;
+    P.pair_y = d_py;
+    P.pair_out = d_po;
+    P.sx = ps.sx;
+    P.sy = ps.sy;
+    P.w65 = c.w65.as<double>();
+    P.rho_tab = dp == 0 ? c.tab.as<double>() : nullptr;
+    P.tab_stride = tab_elems;
+    P.dim = ps.dim;
+    P.order = order;
+    P.rows = rows;
+    P.cols = cols;
+    P.bands = bands;
+    P.npairs = static_cast<int>(npairs);
+    P.group = static_cast<int>(group);
+    P.slots = static_cast<int>(slots);
+    P.flags = flags;
+    P.abuf = bands > 1 ? c.abuf.as<double>() : nullptr;
+    P.prog = c.prog.as<unsigned long long>();
+    P.queue = c.queue.as<unsigned>();
+    P.values = o.d_values;
+    P.err = o.d_err;
+    P.maxrho = o.d_maxrho;
+    P.grid = o.d_grid;
+    P.diag = o.d_diag;
+    P.grid_stride = o.grid_stride;
+    P.diag_stride = o.diag_stride;
+    StatRec rec{};
+    rec.tiles = static_cast<double>(npairs) * rows * cols;
+    rec.flops = rec.tiles * flops_per_tile(order, ps.dim);
+    if (int rc = record_start(c, &rec, st)) return rc;
+    SK_CUDA(sweep_launch(ntempl, dp, blocks, c.stream(), P));
+    if (int rc = record_end(c, &rec, st)) return rc;
+    ++c.sweep_launches;
+  }
+  return SK_OK;
+}
+
+// Per-pair truncation order (wavefront.cpp:206-221 / gram.cpp:57-64).
+// estimate_order is monotone in max|rho| and never below 8, so when the
+// Cauchy-Schwarz bound U >= max|rho| already yields N = 8 that is the exact
+// answer; only the other pairs pay for the O(l^2 d) exact scan.
+int adaptive_orders(Ctx& c, const PairSet& ps, const std::vector<double>& h_sqn_x,
+                    const std::vector<double>& h_sqn_y, const std::vector<uint32_t>& px,
+                    const std::vector<uint32_t>& py, double tol, std::vector<int>& orders, std::vector<int>& conv,
+                    sk_status* st) {
+  const size_t np = px.size();
+  orders.assign(np, 8);
+  conv.assign(np, 1);
+  const double slack = 1e-10 + 8.0 * (ps.dim + 2) * std::ldexp(1.0, -53);
+  std::vector<uint32_t> sx_list, sy_list, idx;
+  for (size_t k = 0; k < np; ++k) {
+    const double u = std::sqrt(h_sqn_x[px[k]]) * std::sqrt(h_sqn_y[py[k]]) * (1.0 + slack);
+    int ord = 0, cv = 0;
+    if (std::isfinite(u)) host_estimate_order(u, tol, &ord, &cv);
+    if (std::isfinite(u) && ord == 8 && cv) continue;
+    sx_list.push_back(px[k]);
+    sy_list.push_back(py[k]);
+    idx.push_back(static_cast<uint32_t>(k));
+  }
+  if (idx.empty()) return SK_OK;
+  const size_t ns = idx.size();
+  SK_CUDA(c.pairs.ensure(2 * ns * sizeof(uint32_t)));
+  SK_CUDA(c.scan.ensure(ns * sizeof(unsigned long long)));
+  uint32_t* d_px = c.pairs.as<uint32_t>();
+  uint32_t* d_py = d_px + ns;
+  SK_CUDA(cudaMemcpyAsync(d_px, sx_list.data(), ns * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(d_py, sy_list.data(), ns * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemsetAsync(c.scan.p, 0, ns * sizeof(unsigned long long), c.stream()));
+  SK_CUDA(launch_maxrho_scan(ps.d_xinc, ps.d_yinc, d_px, d_py, ns, ps.sx, ps.sy, ps.rows, ps.cols, ps.dim,
+                             c.scan.as<unsigned long long>(), c.stream()));
+  ++c.aux_launches;
+  std::vector<unsigned long long> bits(ns);
+  SK_CUDA(cudaMemcpyAsync(bits.data(), c.scan.p, ns * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  for (size_t t = 0; t < ns; ++t) {
+    double mr;
+    std::memcpy(&mr, &bits[t], sizeof mr);
+    if (mr < 0.0 || !std::isfinite(mr))
+      return set_status(st, SK_INVALID_ARGUMENT, 0, 0,
+                        "estimate_order: max_abs_rho must be finite and nonnegative");
+    host_estimate_order(mr, tol, &orders[idx[t]], &conv[idx[t]]);
+  }
+  return SK_OK;
+}
+
+// decode an error key into the reference's exception contract
+int decode_err(unsigned long long key, sk_status* st, const double* xinc_host, const double* yinc_host,
+               size_t dim) {
+  const unsigned code = static_cast<unsigned>(key & 3ull);
+  const uint64_t i = (key >> 2) & 0x3fffffffull;
+  const uint64_t d = key >> 32;
+  const uint64_t j = d - i;
+  if (code == kErrDelta) {
+    double delta = std::numeric_limits<double>::quiet_NaN();
+    if (xinc_host && yinc_host) {
+      delta = 0.0;
+      for (size_t c = 0; c < dim; ++c) delta += xinc_host[j * dim + c] * yinc_host[i * dim + c];
+    }
+    return set_status(st, SK_NUMERIC_OVERFLOW, j + 1, i + 1,
+                      "increment product %f on tile (%llu, %llu) exceeds double range at any order; rescale "
+                      "the inputs",
+                      delta, static_cast<unsigned long long>(j + 1), static_cast<unsigned long long>(i + 1));
+  }
+  if (code == kErrCorner)
+    return set_status(st, SK_INCONSISTENT_BOUNDARY, j + 1, i + 1,
+                      "boundary series disagree at the shared corner on tile (%llu, %llu)",
+                      static_cast<unsigned long long>(j + 1), static_cast<unsigned long long>(i + 1));
+  return set_status(st, SK_NUMERIC_OVERFLOW, j + 1, i + 1,
+                    "non-finite series on tile (%llu, %llu); rescale the inputs or reduce the order",
+                    static_cast<unsigned long long>(j + 1), static_cast<unsigned long long>(i + 1));
+}
+
+// Pairwise core on device-resident raw series.  values: device, npairs.
+struct PairwiseResult {
+  std::vector<int> orders, conv;
+  std::vector<unsigned long long> err;
+  std::vector<unsigned long long> maxr;
+};
+
+int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw, size_t ly, size_t npairs,
+                  size_t dim, int adaptive, int order, double tol, uint32_t flags, double* d_values,
+                  bool want_maxrho, double* d_grid, double* d_diag, PairwiseResult& res, sk_status* st) {
+  const size_t cx = lx - 1, cy = ly - 1;
+  SK_CUDA(c.xinc.ensure(npairs * cx * dim * sizeof(double)));
+  SK_CUDA(c.yinc.ensure(npairs * cy * dim * sizeof(double)));
+  SK_CUDA(launch_increments(d_xraw, npairs, lx, dim, c.xinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(d_yraw, npairs, ly, dim, c.yinc.as<double>(), c.stream()));
+  c.aux_launches += 2;
+  PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), cx * dim, cy * dim, static_cast<int>(cy),
+             static_cast<int>(cx), static_cast<int>(dim)};
+  std::vector<uint32_t> px(npairs), py(npairs), pout(npairs);
+  for (size_t k = 0; k < npairs; ++k) px[k] = py[k] = pout[k] = static_cast<uint32_t>(k);
+  if (adaptive) {
+    SK_CUDA(c.sqn.ensure(2 * npairs * sizeof(double)));
+    SK_CUDA(launch_max_sqnorm(ps.d_xinc, npairs, cx, dim, c.sqn.as<double>(), c.stream()));
+    SK_CUDA(launch_max_sqnorm(ps.d_yinc, npairs, cy, dim, c.sqn.as<double>() + npairs, c.stream()));
+    c.aux_launches += 2;
+    std::vector<double> h(2 * npairs);
+    SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, 2 * npairs * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    SK_CUDA(cudaStreamSynchronize(c.stream()));
+    std::vector<double> hx(h.begin(), h.begin() + npairs), hy(h.begin() + npairs, h.end());
+    if (int rc = adaptive_orders(c, ps, hx, hy, px, py, tol, res.orders, res.conv, st)) return rc;
+  } else {
+    res.orders.assign(npairs, order);
+    res.conv.assign(npairs, 1);
+  }
+  SK_CUDA(c.err.ensure(npairs * sizeof(unsigned long long)));
+  SK_CUDA(cudaMemsetAsync(c.err.p, 0xff, npairs * sizeof(unsigned long long), c.stream()));
+  SK_CUDA(cudaMemsetAsync(d_values, 0xff, npairs * sizeof(double), c.stream()));
+  if (want_maxrho) {
+    SK_CUDA(c.maxr.ensure(npairs * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemsetAsync(c.maxr.p, 0, npairs * sizeof(unsigned long long), c.stream()));
+  }
+  Outputs o{d_values, c.err.as<unsigned long long>(), want_maxrho ? c.maxr.as<unsigned long long>() : nullptr,
+            d_grid, d_diag, lx * ly, std::min(cx, cy)};
+  // one sweep per distinct order
+  std::vector<int> distinct(res.orders.begin(), res.orders.end());
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  for (int ord : distinct) {
+    std::vector<uint32_t> gx, gy, go;
+    for (size_t k = 0; k < npairs; ++k)
+      if (res.orders[k] == ord) {
+        gx.push_back(px[k]);
+        gy.push_back(py[k]);
+        go.push_back(pout[k]);
+      }
+    if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags, o, st)) return rc;
+  }
+  res.err.resize(npairs);
+  SK_CUDA(cudaMemcpyAsync(res.err.data(), c.err.p, npairs * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c.stream()));
+  if (want_maxrho) {
+    res.maxr.resize(npairs);
+    SK_CUDA(cudaMemcpyAsync(res.maxr.data(), c.maxr.p, npairs * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c.stream()));
+  }
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+// host increments of one tile row/column pair for error messages
+std::vector<double> host_increments(const double* v, size_t len, size_t dim) {
+  std::vector<double> out((len - 1) * dim);
+  for (size_t k = 0; k + 1 < len; ++k)
+    for (size_t c = 0; c < dim; ++c) out[k * dim + c] = v[(k + 1) * dim + c] - v[k * dim + c];
+  return out;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+int sk_abi_version(void) { return SK_ABI_VERSION; }
+
+int sk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int sk_set_device(int device, sk_status* st) {
+  clear_status(st);
+  const int n = sk_device_count();
+  if (device < 0 || device >= n)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "device %d out of range (%d visible)", device, n);
+  t_device = device;
+  return SK_OK;
+}
+
+int sk_set_stream(void* cuda_stream, sk_status* st) {
+  clear_status(st);
+  Ctx* c = nullptr;
+  if (int rc = get_ctx(&c, st)) return rc;
+  c->user = static_cast<cudaStream_t>(cuda_stream);
+  return SK_OK;
+}
+
+int sk_estimate_order(double max_abs_rho, size_t /*length*/, double tol, int* order, int* converged,
+                      sk_status* st) {
+  clear_status(st);
+  if (!(tol > 0.0)) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "estimate_order: tolerance must be positive");
+  if (max_abs_rho < 0.0 || !std::isfinite(max_abs_rho))
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "estimate_order: max_abs_rho must be finite and nonnegative");
+  return host_estimate_order(max_abs_rho, tol, order, converged);
+}
+
+int sk_propagate(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
+                 double* value, uint64_t* peak_live, double* grid, double* diag, sk_status* st) {
+  clear_status(st);
+  if (dim < 1) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate: series dimensions differ");
+  if (lx < 2 || ly < 2) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate: both series need length >= 2");
+  if (order < 1 || order > kMaxOrder)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate: order must lie in [1, 64]");
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  SK_CUDA(c.raw_x.ensure(lx * dim * sizeof(double)));
+  SK_CUDA(c.raw_y.ensure(ly * dim * sizeof(double)));
+  SK_CUDA(c.values.ensure(sizeof(double)));
+  SK_CUDA(cudaMemcpyAsync(c.raw_x.p, x, lx * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(c.raw_y.p, y, ly * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  double* d_grid = nullptr;
+  double* d_diag = nullptr;
+  if (grid) {
+    SK_CUDA(c.grid.ensure(lx * ly * sizeof(double)));
+    d_grid = c.grid.as<double>();
+    SK_CUDA(cudaMemsetAsync(d_grid, 0, lx * ly * sizeof(double), c.stream()));
+    SK_CUDA(launch_grid_init(d_grid, 1, lx, ly, c.stream()));
+  }
+  const size_t nd = std::min(lx, ly) - 1;
+  if (diag) {
+    SK_CUDA(c.diag.ensure(nd * sizeof(double)));
+    d_diag = c.diag.as<double>();
+  }
+  PairwiseResult res;
+  if (int rc = pairwise_core(c, c.raw_x.as<double>(), lx, c.raw_y.as<double>(), ly, 1, dim, 0, order, 1e-12, flags,
+                             c.values.as<double>(), false, d_grid, d_diag, res, st))
+    return rc;
+  if (res.err[0] != ~0ull) {
+    const auto xi = host_increments(x, lx, dim);
+    const auto yi = host_increments(y, ly, dim);
+    return decode_err(res.err[0], st, xi.data(), yi.data(), dim);
+  }
+  SK_CUDA(cudaMemcpy(value, c.values.p, sizeof(double), cudaMemcpyDeviceToHost));
+  if (grid) SK_CUDA(cudaMemcpy(grid, d_grid, lx * ly * sizeof(double), cudaMemcpyDeviceToHost));
+  if (diag) SK_CUDA(cudaMemcpy(diag, d_diag, nd * sizeof(double), cudaMemcpyDeviceToHost));
+  if (peak_live) *peak_live = peak_live_closed_form(ly - 1, lx - 1);
+  return SK_OK;
+}
+
+int sk_max_abs_rho(const double* x, size_t lx, const double* y, size_t ly, size_t dim, double* out, sk_status* st) {
+  clear_status(st);
+  if (dim < 1 || lx < 2 || ly < 2)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "increments: a single point has no increments");
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  SK_CUDA(c.raw_x.ensure(lx * dim * sizeof(double)));
+  SK_CUDA(c.raw_y.ensure(ly * dim * sizeof(double)));
+  SK_CUDA(c.xinc.ensure((lx - 1) * dim * sizeof(double)));
+  SK_CUDA(c.yinc.ensure((ly - 1) * dim * sizeof(double)));
+  SK_CUDA(cudaMemcpyAsync(c.raw_x.p, x, lx * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(c.raw_y.p, y, ly * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(launch_increments(c.raw_x.as<double>(), 1, lx, dim, c.xinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(c.raw_y.as<double>(), 1, ly, dim, c.yinc.as<double>(), c.stream()));
+  SK_CUDA(c.pairs.ensure(2 * sizeof(uint32_t)));
+  SK_CUDA(cudaMemsetAsync(c.pairs.p, 0, 2 * sizeof(uint32_t), c.stream()));
+  SK_CUDA(c.scan.ensure(sizeof(unsigned long long)));
+  SK_CUDA(cudaMemsetAsync(c.scan.p, 0, sizeof(unsigned long long), c.stream()));
+  uint32_t* d_p = c.pairs.as<uint32_t>();
+  SK_CUDA(launch_maxrho_scan(c.xinc.as<double>(), c.yinc.as<double>(), d_p, d_p + 1, 1, 0, 0,
+                             static_cast<int>(ly - 1), static_cast<int>(lx - 1), static_cast<int>(dim),
+                             c.scan.as<unsigned long long>(), c.stream()));
+  c.aux_launches += 3;
+  unsigned long long bits = 0;
+  SK_CUDA(cudaMemcpyAsync(&bits, c.scan.p, sizeof bits, cudaMemcpyDeviceToHost, c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  std::memcpy(out, &bits, sizeof(double));
+  return SK_OK;
+}
+
+static int step_tile_common(bool fast, double delta, const double* alpha, const double* beta, int order,
+                            double* out_alpha, double* out_beta, double* total, sk_status* st) {
+  clear_status(st);
+  if (order < 0 || order > kMaxOrder)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "step_tile: order must lie in [0, 64]");
+  if (fast && (order < 1 || order > kMaxRegOrder))
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "step_tile_fast: order must lie in [1, 16]");
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  const int n = order + 1;
+  std::vector<double> in(2 * (kMaxOrder + 1), 0.0), out(2 * (kMaxOrder + 1) + 1, 0.0);
+  std::copy(alpha, alpha + n, in.begin());
+  std::copy(beta, beta + n, in.begin() + (kMaxOrder + 1));
+  SK_CUDA(c.tile_io.ensure((in.size() + out.size()) * sizeof(double)));
+  double* d_in = c.tile_io.as<double>();
+  double* d_out = d_in + in.size();
+  SK_CUDA(cudaMemcpyAsync(d_in, in.data(), in.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  if (fast) {
+    SK_CUDA(launch_step_tile_fast(delta, order, d_in, d_out, c.stream()));
+  } else {
+    SK_CUDA(launch_step_tile_literal(delta, order, c.w65.as<double>(), d_in, d_out, c.stream()));
+  }
+  ++c.aux_launches;
+  SK_CUDA(cudaMemcpyAsync(out.data(), d_out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  std::copy(out.begin(), out.begin() + n, out_alpha);
+  std::copy(out.begin() + (kMaxOrder + 1), out.begin() + (kMaxOrder + 1) + n, out_beta);
+  if (total) *total = out[2 * (kMaxOrder + 1)];
+  return SK_OK;
+}
+
+int sk_step_tile(double delta, const double* alpha, const double* beta, int order, double* out_alpha,
+                 double* out_beta, double* total, sk_status* st) {
+  return step_tile_common(false, delta, alpha, beta, order, out_alpha, out_beta, total, st);
+}
+
+int sk_step_tile_fast(double delta, const double* alpha, const double* beta, int order, double* out_alpha,
+                      double* out_beta, double* total, sk_status* st) {
+  return step_tile_common(true, delta, alpha, beta, order, out_alpha, out_beta, total, st);
+}
+
+static int pairwise_validate(size_t lx, size_t ly, size_t dim, int adaptive, int order, double tol, sk_status* st) {
+  if (dim < 1) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "pairwise: dimension must be >= 1");
+  if (lx < 2 || ly < 2) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate: both series need length >= 2");
+  if (adaptive) {
+    if (!(tol > 0.0)) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "adaptive tolerance must be positive");
+  } else if (order < 1 || order > kMaxOrder) {
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate: order must lie in [1, 64]");
+  }
+  return SK_OK;
+}
+
+static void fill_pair_outputs(const PairwiseResult& res, size_t npairs, double* values, int* orders,
+                              int* converged, double* max_abs_rho, sk_status* per_pair, const double* xs,
+                              size_t lx, const double* ys, size_t ly, size_t dim) {
+  for (size_t k = 0; k < npairs; ++k) {
+    if (orders) orders[k] = res.orders[k];
+    if (converged) converged[k] = res.conv[k];
+    if (max_abs_rho && !res.maxr.empty()) std::memcpy(&max_abs_rho[k], &res.maxr[k], sizeof(double));
+    if (res.err[k] != ~0ull) {
+      if (values) values[k] = std::numeric_limits<double>::quiet_NaN();
+      if (per_pair) {
+        std::vector<double> xi, yi;
+        if (xs && ys) {
+          xi = host_increments(xs + k * lx * dim, lx, dim);
+          yi = host_increments(ys + k * ly * dim, ly, dim);
+        }
+        decode_err(res.err[k], &per_pair[k], xs ? xi.data() : nullptr, ys ? yi.data() : nullptr, dim);
+      }
+    } else if (per_pair) {
+      clear_status(&per_pair[k]);
+    }
+  }
+}
+
+int sk_pairwise(const double* xs, size_t lx, const double* ys, size_t ly, size_t npairs, size_t dim, int adaptive,
+                int order, double tol, uint32_t flags, double* values, int* orders, int* converged,
+                double* max_abs_rho, sk_status* per_pair, sk_status* st) {
+  clear_status(st);
+  if (npairs == 0) return SK_OK;
+  if (int rc = pairwise_validate(lx, ly, dim, adaptive, order, tol, st)) return rc;
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  SK_CUDA(c.raw_x.ensure(npairs * lx * dim * sizeof(double)));
+  SK_CUDA(c.raw_y.ensure(npairs * ly * dim * sizeof(double)));
+  SK_CUDA(c.values.ensure(npairs * sizeof(double)));
+  SK_CUDA(cudaMemcpyAsync(c.raw_x.p, xs, npairs * lx * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(c.raw_y.p, ys, npairs * ly * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  PairwiseResult res;
+  if (int rc = pairwise_core(c, c.raw_x.as<double>(), lx, c.raw_y.as<double>(), ly, npairs, dim, adaptive, order,
+                             tol, flags, c.values.as<double>(), adaptive && max_abs_rho, nullptr, nullptr, res, st))
+    return rc;
+  SK_CUDA(cudaMemcpy(values, c.values.p, npairs * sizeof(double), cudaMemcpyDeviceToHost));
+  fill_pair_outputs(res, npairs, values, orders, converged, max_abs_rho, per_pair, xs, lx, ys, ly, dim);
+  return SK_OK;
+}
+
+int sk_pairwise_device(const double* d_xs, size_t lx, const double* d_ys, size_t ly, size_t npairs, size_t dim,
+                       int adaptive, int order, double tol, uint32_t flags, double* d_values, int* orders,
+                       int* converged, sk_status* per_pair, sk_status* st) {
+  clear_status(st);
+  if (npairs == 0) return SK_OK;
+  if (int rc = pairwise_validate(lx, ly, dim, adaptive, order, tol, st)) return rc;
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  PairwiseResult res;
+  if (int rc = pairwise_core(*cp, d_xs, lx, d_ys, ly, npairs, dim, adaptive, order, tol, flags, d_values, false,
+                             nullptr, nullptr, res, st))
+    return rc;
+  fill_pair_outputs(res, npairs, nullptr, orders, converged, nullptr, per_pair, nullptr, lx, nullptr, ly, dim);
+  return SK_OK;
+}
+
+int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
+            uint32_t flags, int scan_products, size_t shard, size_t nshards, double* values, int* orders,
+            double* pair_max, double* max_product, int* converged, sk_status* entry_status, sk_status* st) {
+  clear_status(st);
+  if (m == 0) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: family must be nonempty");
+  if (dim < 1) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: dimension must be >= 1");
+  if (len < 2) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: common length must be >= 2");
+  if (nshards < 1 || shard >= nshards)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: shard %zu out of range [0, %zu)", shard, nshards);
+  if (adaptive ? !(tol > 0.0) : (order < 1 || order > kMaxOrder))
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, adaptive ? "adaptive tolerance must be positive"
+                                                             : "propagate: order must lie in [1, 64]");
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  const size_t total_pairs = m * (m + 1) / 2;
+  const size_t t0 = total_pairs * shard / nshards, t1 = total_pairs * (shard + 1) / nshards;
+  const size_t np = t1 - t0;
+  for (size_t k = 0; k < m * m; ++k) {
+    if (values) values[k] = std::numeric_limits<double>::quiet_NaN();
+    if (orders) orders[k] = 0;
+    if (pair_max) pair_max[k] = 0.0;
+    if (entry_status) clear_status(&entry_status[k]);
+  }
+  if (max_product) *max_product = 0.0;
+  if (converged) *converged = 1;
+  if (np == 0) return SK_OK;
+  // upper-triangle pairs (i <= j), row-major (gram.cpp:39-42)
+  std::vector<uint32_t> pi(np), pj(np), pout(np);
+  {
+    size_t t = 0, i = 0, j = 0;
+    // locate t0
+    size_t row_start = 0;
+    while (i < m && row_start + (m - i) <= t0) {
+      row_start += m - i;
+      ++i;
+    }
+    j = i + (t0 - row_start);
+    for (t = 0; t < np; ++t) {
+      pi[t] = static_cast<uint32_t>(i);
+      pj[t] = static_cast<uint32_t>(j);
+      pout[t] = static_cast<uint32_t>(t);
+      if (++j == m) {
+        ++i;
+        j = i;
+      }
+    }
+  }
+  const size_t cnt = len - 1;
+  SK_CUDA(c.raw_x.ensure(m * len * dim * sizeof(double)));
+  SK_CUDA(c.xinc.ensure(m * cnt * dim * sizeof(double)));
+  SK_CUDA(c.values.ensure(np * sizeof(double)));
+  SK_CUDA(cudaMemcpyAsync(c.raw_x.p, family, m * len * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(launch_increments(c.raw_x.as<double>(), m, len, dim, c.xinc.as<double>(), c.stream()));
+  ++c.aux_launches;
+  // propagate(padded[i], padded[j]): x = member i (columns), y = member j (rows)
+  PairSet ps{c.xinc.as<double>(), c.xinc.as<double>(), cnt * dim, cnt * dim, static_cast<int>(cnt),
+             static_cast<int>(cnt), static_cast<int>(dim)};
+  std::vector<int> ords, conv;
+  if (adaptive) {
+    SK_CUDA(c.sqn.ensure(m * sizeof(double)));
+    SK_CUDA(launch_max_sqnorm(ps.d_xinc, m, cnt, dim, c.sqn.as<double>(), c.stream()));
+    ++c.aux_launches;
+    std::vector<double> h(m);
+    SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, m * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    SK_CUDA(cudaStreamSynchronize(c.stream()));
+    if (int rc = adaptive_orders(c, ps, h, h, pi, pj, tol, ords, conv, st)) return rc;
+  } else {
+    ords.assign(np, order);
+    conv.assign(np, 1);
+  }
+  const bool want_max = scan_products != 0;
+  SK_CUDA(c.err.ensure(np * sizeof(unsigned long long)));
+  SK_CUDA(cudaMemsetAsync(c.err.p, 0xff, np * sizeof(unsigned long long), c.stream()));
+  SK_CUDA(cudaMemsetAsync(c.values.p, 0xff, np * sizeof(double), c.stream()));
+  if (want_max) {
+    SK_CUDA(c.maxr.ensure(np * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemsetAsync(c.maxr.p, 0, np * sizeof(unsigned long long), c.stream()));
+  }
+  Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(),
+            want_max ? c.maxr.as<unsigned long long>() : nullptr, nullptr, nullptr, 0, 0};
+  std::vector<int> distinct(ords.begin(), ords.end());
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  for (int ord : distinct) {
+    std::vector<uint32_t> gx, gy, go;
+    for (size_t k = 0; k < np; ++k)
+      if (ords[k] == ord) {
+        gx.push_back(pi[k]);
+        gy.push_back(pj[k]);
+        go.push_back(pout[k]);
+      }
+    if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags, o, st)) return rc;
+  }
+  std::vector<double> hv(np);
+  std::vector<unsigned long long> he(np), hm(want_max ? np : 0);
+  SK_CUDA(cudaMemcpyAsync(hv.data(), c.values.p, np * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(he.data(), c.err.p, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream()));
+  if (want_max)
+    SK_CUDA(cudaMemcpyAsync(hm.data(), c.maxr.p, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  SK_CUDA(cudaGetLastError());
+  double best = 0.0;
+  int first_fatal = -1;
+  for (size_t t = 0; t < np; ++t) {
+    const size_t i = pi[t], j = pj[t];
+    double v = hv[t];
+    if (he[t] != ~0ull) {
+      v = std::numeric_limits<double>::quiet_NaN();
+      if ((he[t] & 3ull) == kErrCorner) {
+        if (first_fatal < 0) first_fatal = static_cast<int>(t);
+      } else if (entry_status) {
+        const auto xi = host_increments(family + i * len * dim, len, dim);
+        const auto yi = host_increments(family + j * len * dim, len, dim);
+        decode_err(he[t], &entry_status[i * m + j], xi.data(), yi.data(), dim);
+      }
+    }
+    if (values) {
+      values[i * m + j] = v;
+      values[j * m + i] = v;
+    }
+    if (orders) {
+      orders[i * m + j] = ords[t];
+      orders[j * m + i] = ords[t];
+    }
+    if (want_max) {
+      double mr;
+      std::memcpy(&mr, &hm[t], sizeof mr);
+      if (pair_max) {
+        pair_max[i * m + j] = mr;
+        pair_max[j * m + i] = mr;
+      }
+      if (best < mr) best = mr;
+    }
+    if (converged && !conv[t]) *converged = 0;
+  }
+  if (max_product) *max_product = best;
+  if (first_fatal >= 0) return decode_err(he[first_fatal], st, nullptr, nullptr, dim);
+  return SK_OK;
+}
+
+int sk_stats_enable(int enable) {
+  sk_status st;
+  Ctx* c = nullptr;
+  if (get_ctx(&c, &st)) return st.code;
+  c->stats_on = enable != 0;
+  return SK_OK;
+}
+
+int sk_stats_reset(void) {
+  sk_status st;
+  Ctx* c = nullptr;
+  if (get_ctx(&c, &st)) return st.code;
+  cudaStreamSynchronize(c->stream());
+  for (auto& r : c->stats) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  c->stats.clear();
+  c->sweep_launches = c->aux_launches = 0;
+  c->done_ms = c->done_tiles = c->done_flops = 0.0;
+  return SK_OK;
+}
+
+int sk_stats_get(sk_stats* out) {
+  sk_status st;
+  Ctx* c = nullptr;
+  if (get_ctx(&c, &st)) return st.code;
+  for (auto& r : c->stats) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    c->done_ms += ms;
+    c->done_tiles += r.tiles;
+    c->done_flops += r.flops;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  c->stats.clear();
+  out->sweep_launches = c->sweep_launches;
+  out->aux_launches = c->aux_launches;
+  out->sweep_ms = c->done_ms;
+  out->tiles = c->done_tiles;
+  out->tile_flops = c->done_flops;
+  return SK_OK;
+}
+
+int sk_release(void) {
+  if (t_ctx) {
+    cudaStreamSynchronize(t_ctx->stream());
+    t_ctx.reset();
+  }
+  return SK_OK;
+}
+
+}  // extern "C"
