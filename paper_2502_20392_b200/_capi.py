@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsigker_b200.so")
+LIB_PATH = os.environ.get("SIGKER_B200_LIB", os.path.join(_HERE, "libsigker_b200.so"))
 
 SK_OK = 0
 SK_INVALID_ARGUMENT = 1

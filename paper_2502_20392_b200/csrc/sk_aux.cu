@@ -11,29 +11,37 @@
 
 namespace skb {
 
-// time_series.cpp:32-42: dz_k = z_{k+1} - z_k, (len-1) x dim row-major per series.
-__global__ void increments_kernel(const double* __restrict__ v, size_t nseries, size_t len, size_t dim,
+// time_series.cpp:32-42: dz_k = z_{k+1} - z_k.  Device layout per series:
+// `len` rows of `ld` doubles -- row 0 is zeros, row k+1 holds dz_k, columns
+// >= dim are zero -- so the sweep's row -1 reads a zero vector and every
+// row is 16-byte aligned for ld even.
+__global__ void increments_kernel(const double* __restrict__ v, size_t nseries, size_t len, size_t dim, size_t ld,
                                   double* __restrict__ out) {
-  const size_t per = (len - 1) * dim;
+  const size_t per = len * ld;
   const size_t total = nseries * per;
   for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t s = t / per;
-    const size_t k = t - s * per;
-    const double* src = v + s * len * dim + k;
-    out[t] = src[dim] - src[0];
+    const size_t e = t - s * per;
+    const size_t row = e / ld, c = e - row * ld;
+    double val = 0.0;
+    if (row > 0 && c < dim) {
+      const double* src = v + s * len * dim + (row - 1) * dim + c;
+      val = src[dim] - src[0];
+    }
+    out[t] = val;
   }
 }
 
 // Per series: max_k sum_c dz_k[c]^2 (only feeds the Cauchy-Schwarz upper
 // bound of max|rho|, so its rounding is covered by the bound's slack).
-__global__ void max_sqnorm_kernel(const double* __restrict__ inc, size_t count, size_t dim,
+__global__ void max_sqnorm_kernel(const double* __restrict__ inc, size_t count, size_t dim, size_t ld,
                                   double* __restrict__ out) {
-  const double* s = inc + blockIdx.x * count * dim;
+  const double* s = inc + blockIdx.x * (count + 1) * ld + ld;
   double best = 0.0;
   for (size_t k = threadIdx.x; k < count; k += blockDim.x) {
     double acc = 0.0;
-    for (size_t c = 0; c < dim; ++c) acc = fma(s[k * dim + c], s[k * dim + c], acc);
+    for (size_t c = 0; c < dim; ++c) acc = fma(s[k * ld + c], s[k * ld + c], acc);
     best = fmax(best, acc);
   }
   __shared__ double red[32];
@@ -55,20 +63,20 @@ __global__ void max_sqnorm_kernel(const double* __restrict__ inc, size_t count, 
 template <int DP>
 __global__ void maxrho_scan_kernel(const double* __restrict__ xinc, const double* __restrict__ yinc,
                                    const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
-                                   unsigned long long sx, unsigned long long sy, int rows, int cols, int dim,
+                                   unsigned long long sx, unsigned long long sy, int rows, int cols, int dim, int ld,
                                    unsigned long long* __restrict__ out) {
   const int pr = blockIdx.y;
-  const double* xs = xinc + px[pr] * sx;
-  const double* ys = yinc + py[pr] * sy;
+  const double* xs = xinc + px[pr] * sx + ld;
+  const double* ys = yinc + py[pr] * sy + ld;
   double best = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
-    const double* yr = ys + static_cast<size_t>(i) * dim;
+    const double* yr = ys + static_cast<size_t>(i) * ld;
     if constexpr (DP > 0) {
       double yv[DP];
 #pragma unroll
       for (int c = 0; c < DP; ++c) yv[c] = (c < dim) ? yr[c] : 0.0;
       for (int j = 0; j < cols; ++j) {
-        const double* xr = xs + static_cast<size_t>(j) * dim;
+        const double* xr = xs + static_cast<size_t>(j) * ld;
         double xv[DP];
 #pragma unroll
         for (int c = 0; c < DP; ++c) xv[c] = (c < dim) ? __ldg(xr + c) : 0.0;
@@ -77,7 +85,7 @@ __global__ void maxrho_scan_kernel(const double* __restrict__ xinc, const double
       }
     } else {
       for (int j = 0; j < cols; ++j) {
-        const double* xr = xs + static_cast<size_t>(j) * dim;
+        const double* xr = xs + static_cast<size_t>(j) * ld;
         double acc = __dmul_rn(__ldg(xr), yr[0]);
         for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + c), yr[c]));
         const double a = fabs(acc);
@@ -97,10 +105,10 @@ __global__ void maxrho_scan_kernel(const double* __restrict__ xinc, const double
 __global__ void rho_table_kernel(const double* __restrict__ xinc, const double* __restrict__ yinc,
                                  const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
                                  unsigned long long sx, unsigned long long sy, int rows, int cols, int bands,
-                                 int dim, double* __restrict__ tab, unsigned long long tab_stride) {
+                                 int dim, int ld, double* __restrict__ tab, unsigned long long tab_stride) {
   const int pr = blockIdx.y;
-  const double* xs = xinc + px[pr] * sx;
-  const double* ys = yinc + py[pr] * sy;
+  const double* xs = xinc + px[pr] * sx + ld;
+  const double* ys = yinc + py[pr] * sy + ld;
   double* t = tab + pr * tab_stride;
   const size_t steps = static_cast<size_t>(cols) + 31;
   const size_t total = static_cast<size_t>(bands) * steps * 32;
@@ -114,8 +122,8 @@ __global__ void rho_table_kernel(const double* __restrict__ xinc, const double* 
     const int j = s - lane;
     double v = 0.0;
     if (i < rows && j >= 0 && j < cols) {
-      const double* xr = xs + static_cast<size_t>(j) * dim;
-      const double* yr = ys + static_cast<size_t>(i) * dim;
+      const double* xr = xs + static_cast<size_t>(j) * ld;
+      const double* yr = ys + static_cast<size_t>(i) * ld;
       double acc = __dmul_rn(__ldg(xr), __ldg(yr));
       for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + c), __ldg(yr + c)));
       v = acc;
@@ -179,49 +187,50 @@ static int grid_for(size_t work, int threads) {
   return static_cast<int>(g);
 }
 
-cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, double* out,
+cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, size_t ld, double* out,
                               cudaStream_t st) {
-  const size_t work = nseries * (len - 1) * dim;
+  const size_t work = nseries * len * ld;
   if (work == 0) return cudaSuccess;
-  increments_kernel<<<grid_for(work, 256), 256, 0, st>>>(v, nseries, len, dim, out);
+  increments_kernel<<<grid_for(work, 256), 256, 0, st>>>(v, nseries, len, dim, ld, out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, double* out,
+cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, size_t ld, double* out,
                               cudaStream_t st) {
   if (nseries == 0) return cudaSuccess;
-  max_sqnorm_kernel<<<static_cast<unsigned>(nseries), 256, 0, st>>>(inc, count, dim, out);
+  max_sqnorm_kernel<<<static_cast<unsigned>(nseries), 256, 0, st>>>(inc, count, dim, ld, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                                size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
-                               int dim, unsigned long long* out, cudaStream_t st) {
+                               int dim, int ld, unsigned long long* out, cudaStream_t st) {
   if (npairs == 0) return cudaSuccess;
   const int threads = 128;
   const int bx = (rows + threads - 1) / threads;
   const dim3 grid(bx, static_cast<unsigned>(npairs));
   const int dp = pick_dp(dim);
   switch (dp) {
-    case 2: maxrho_scan_kernel<2><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
-    case 4: maxrho_scan_kernel<4><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
-    case 8: maxrho_scan_kernel<8><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
-    case 16: maxrho_scan_kernel<16><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
-    default: maxrho_scan_kernel<0><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, out); break;
+    case 2: maxrho_scan_kernel<2><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, ld, out); break;
+    case 4: maxrho_scan_kernel<4><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, ld, out); break;
+    case 8: maxrho_scan_kernel<8><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, ld, out); break;
+    case 16: maxrho_scan_kernel<16><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, ld, out); break;
+    default: maxrho_scan_kernel<0><<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, ld, out); break;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
-                             int bands, int dim, double* tab, unsigned long long tab_stride, cudaStream_t st) {
+                             int bands, int dim, int ld, double* tab, unsigned long long tab_stride,
+                             cudaStream_t st) {
   if (npairs == 0) return cudaSuccess;
   const size_t per = static_cast<size_t>(bands) * (cols + 31) * 32;
   const int threads = 256;
   size_t bx = (per + threads - 1) / threads;
   if (bx > 4096) bx = 4096;
   const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(npairs));
-  rho_table_kernel<<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, bands, dim, tab, tab_stride);
+  rho_table_kernel<<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, bands, dim, ld, tab, tab_stride);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,9 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "sigker_b200.h"
 #include "sk_internal.h"
 #include "sk_sweep.cuh"
@@ -52,6 +55,25 @@ int cuda_fail(sk_status* st, cudaError_t e, const char* where) {
     cudaError_t e_ = (call);                                \
     if (e_ != cudaSuccess) return cuda_fail(st, e_, #call); \
   } while (0)
+
+// ----------------------------------------------------------------- tracing
+// SK_TRACE=1: host wall-clock per phase on stderr (diagnostics only).
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_TRACE");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
+struct Tracer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!trace_on()) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sk] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 // ------------------------------------------------------------ host tables
 const double* host_factorials() {
@@ -217,8 +239,8 @@ int get_ctx(Ctx** out, sk_status* st) {
 struct PairSet {
   const double* d_xinc;
   const double* d_yinc;
-  unsigned long long sx, sy;  // elements between series
-  int rows, cols, dim;
+  unsigned long long sx, sy;  // elements between series (len * ld)
+  int rows, cols, dim, ld;    // ld: row stride of the increments (inc_ld)
 };
 
 struct Outputs {
@@ -263,10 +285,14 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   const int rows = ps.rows, cols = ps.cols;
   const int bands = (rows + 31) / 32;
   int bps = 0;
-  SK_CUDA(sweep_occupancy(ntempl, dp, &bps));
+  const bool exact = o.d_maxrho != nullptr;
+  const bool extras = o.d_grid != nullptr || o.d_diag != nullptr;
+  SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, &bps));
   if (bps < 1) return set_status(st, SK_CUDA_ERROR, 0, 0, "sweep kernel cannot be resident (occupancy 0)");
+  Tracer tr;
   size_t free_b = 0, total_b = 0;
   SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  tr.mark("  occupancy+memgetinfo");
 
   // large d: per-pair skewed rho tables, pairs chunked to a memory budget
   const size_t tab_elems = dp == 0 ? static_cast<size_t>(bands) * (cols + 31) * 32 : 0;
@@ -310,7 +336,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     if (dp == 0) {
       SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
       SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, bands, ps.dim,
-                               c.tab.as<double>(), tab_elems, c.stream()));
+                               ps.ld, c.tab.as<double>(), tab_elems, c.stream()));
       ++c.aux_launches;
     }
     SweepParams P{};
@@ -343,11 +369,12 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.diag = o.d_diag;
     P.grid_stride = o.grid_stride;
     P.diag_stride = o.diag_stride;
+
     StatRec rec{};
     rec.tiles = static_cast<double>(npairs) * rows * cols;
     rec.flops = rec.tiles * flops_per_tile(order, ps.dim);
     if (int rc = record_start(c, &rec, st)) return rc;
-    SK_CUDA(sweep_launch(ntempl, dp, blocks, c.stream(), P));
+    SK_CUDA(sweep_launch(ntempl, dp, exact, extras, blocks, c.stream(), P));
     if (int rc = record_end(c, &rec, st)) return rc;
     ++c.sweep_launches;
   }
@@ -385,7 +412,7 @@ int adaptive_orders(Ctx& c, const PairSet& ps, const std::vector<double>& h_sqn_
   SK_CUDA(cudaMemcpyAsync(d_px, sx_list.data(), ns * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
   SK_CUDA(cudaMemcpyAsync(d_py, sy_list.data(), ns * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
   SK_CUDA(cudaMemsetAsync(c.scan.p, 0, ns * sizeof(unsigned long long), c.stream()));
-  SK_CUDA(launch_maxrho_scan(ps.d_xinc, ps.d_yinc, d_px, d_py, ns, ps.sx, ps.sy, ps.rows, ps.cols, ps.dim,
+  SK_CUDA(launch_maxrho_scan(ps.d_xinc, ps.d_yinc, d_px, d_py, ns, ps.sx, ps.sy, ps.rows, ps.cols, ps.dim, ps.ld,
                              c.scan.as<unsigned long long>(), c.stream()));
   ++c.aux_launches;
   std::vector<unsigned long long> bits(ns);
@@ -440,26 +467,30 @@ struct PairwiseResult {
 int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw, size_t ly, size_t npairs,
                   size_t dim, int adaptive, int order, double tol, uint32_t flags, double* d_values,
                   bool want_maxrho, double* d_grid, double* d_diag, PairwiseResult& res, sk_status* st) {
+  Tracer tr;
   const size_t cx = lx - 1, cy = ly - 1;
-  SK_CUDA(c.xinc.ensure(npairs * cx * dim * sizeof(double)));
-  SK_CUDA(c.yinc.ensure(npairs * cy * dim * sizeof(double)));
-  SK_CUDA(launch_increments(d_xraw, npairs, lx, dim, c.xinc.as<double>(), c.stream()));
-  SK_CUDA(launch_increments(d_yraw, npairs, ly, dim, c.yinc.as<double>(), c.stream()));
+  const size_t ld = inc_ld(dim);
+  SK_CUDA(c.xinc.ensure(npairs * lx * ld * sizeof(double)));
+  SK_CUDA(c.yinc.ensure(npairs * ly * ld * sizeof(double)));
+  SK_CUDA(launch_increments(d_xraw, npairs, lx, dim, ld, c.xinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(d_yraw, npairs, ly, dim, ld, c.yinc.as<double>(), c.stream()));
   c.aux_launches += 2;
-  PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), cx * dim, cy * dim, static_cast<int>(cy),
-             static_cast<int>(cx), static_cast<int>(dim)};
+  PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), lx * ld, ly * ld, static_cast<int>(cy),
+             static_cast<int>(cx), static_cast<int>(dim), static_cast<int>(ld)};
   std::vector<uint32_t> px(npairs), py(npairs), pout(npairs);
   for (size_t k = 0; k < npairs; ++k) px[k] = py[k] = pout[k] = static_cast<uint32_t>(k);
   if (adaptive) {
     SK_CUDA(c.sqn.ensure(2 * npairs * sizeof(double)));
-    SK_CUDA(launch_max_sqnorm(ps.d_xinc, npairs, cx, dim, c.sqn.as<double>(), c.stream()));
-    SK_CUDA(launch_max_sqnorm(ps.d_yinc, npairs, cy, dim, c.sqn.as<double>() + npairs, c.stream()));
+    SK_CUDA(launch_max_sqnorm(ps.d_xinc, npairs, cx, dim, ld, c.sqn.as<double>(), c.stream()));
+    SK_CUDA(launch_max_sqnorm(ps.d_yinc, npairs, cy, dim, ld, c.sqn.as<double>() + npairs, c.stream()));
     c.aux_launches += 2;
     std::vector<double> h(2 * npairs);
     SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, 2 * npairs * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
     SK_CUDA(cudaStreamSynchronize(c.stream()));
+    tr.mark("increments+norms (sync)");
     std::vector<double> hx(h.begin(), h.begin() + npairs), hy(h.begin() + npairs, h.end());
     if (int rc = adaptive_orders(c, ps, hx, hy, px, py, tol, res.orders, res.conv, st)) return rc;
+    tr.mark("adaptive orders");
   } else {
     res.orders.assign(npairs, order);
     res.conv.assign(npairs, 1);
@@ -487,6 +518,7 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
       }
     if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags, o, st)) return rc;
   }
+  tr.mark("sweep launch (async)");
   res.err.resize(npairs);
   SK_CUDA(cudaMemcpyAsync(res.err.data(), c.err.p, npairs * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           c.stream()));
@@ -497,6 +529,7 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
   }
   SK_CUDA(cudaStreamSynchronize(c.stream()));
   SK_CUDA(cudaGetLastError());
+  tr.mark("sweep done (sync)");
   return SK_OK;
 }
 
@@ -603,12 +636,13 @@ int sk_max_abs_rho(const double* x, size_t lx, const double* y, size_t ly, size_
   Ctx& c = *cp;
   SK_CUDA(c.raw_x.ensure(lx * dim * sizeof(double)));
   SK_CUDA(c.raw_y.ensure(ly * dim * sizeof(double)));
-  SK_CUDA(c.xinc.ensure((lx - 1) * dim * sizeof(double)));
-  SK_CUDA(c.yinc.ensure((ly - 1) * dim * sizeof(double)));
+  const size_t ld = inc_ld(dim);
+  SK_CUDA(c.xinc.ensure(lx * ld * sizeof(double)));
+  SK_CUDA(c.yinc.ensure(ly * ld * sizeof(double)));
   SK_CUDA(cudaMemcpyAsync(c.raw_x.p, x, lx * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
   SK_CUDA(cudaMemcpyAsync(c.raw_y.p, y, ly * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
-  SK_CUDA(launch_increments(c.raw_x.as<double>(), 1, lx, dim, c.xinc.as<double>(), c.stream()));
-  SK_CUDA(launch_increments(c.raw_y.as<double>(), 1, ly, dim, c.yinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(c.raw_x.as<double>(), 1, lx, dim, ld, c.xinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(c.raw_y.as<double>(), 1, ly, dim, ld, c.yinc.as<double>(), c.stream()));
   SK_CUDA(c.pairs.ensure(2 * sizeof(uint32_t)));
   SK_CUDA(cudaMemsetAsync(c.pairs.p, 0, 2 * sizeof(uint32_t), c.stream()));
   SK_CUDA(c.scan.ensure(sizeof(unsigned long long)));
@@ -616,7 +650,7 @@ int sk_max_abs_rho(const double* x, size_t lx, const double* y, size_t ly, size_
   uint32_t* d_p = c.pairs.as<uint32_t>();
   SK_CUDA(launch_maxrho_scan(c.xinc.as<double>(), c.yinc.as<double>(), d_p, d_p + 1, 1, 0, 0,
                              static_cast<int>(ly - 1), static_cast<int>(lx - 1), static_cast<int>(dim),
-                             c.scan.as<unsigned long long>(), c.stream()));
+                             static_cast<int>(ld), c.scan.as<unsigned long long>(), c.stream()));
   c.aux_launches += 3;
   unsigned long long bits = 0;
   SK_CUDA(cudaMemcpyAsync(&bits, c.scan.p, sizeof bits, cudaMemcpyDeviceToHost, c.stream()));
@@ -789,19 +823,20 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
     }
   }
   const size_t cnt = len - 1;
+  const size_t ld = inc_ld(dim);
   SK_CUDA(c.raw_x.ensure(m * len * dim * sizeof(double)));
-  SK_CUDA(c.xinc.ensure(m * cnt * dim * sizeof(double)));
+  SK_CUDA(c.xinc.ensure(m * len * ld * sizeof(double)));
   SK_CUDA(c.values.ensure(np * sizeof(double)));
   SK_CUDA(cudaMemcpyAsync(c.raw_x.p, family, m * len * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
-  SK_CUDA(launch_increments(c.raw_x.as<double>(), m, len, dim, c.xinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(c.raw_x.as<double>(), m, len, dim, ld, c.xinc.as<double>(), c.stream()));
   ++c.aux_launches;
   // propagate(padded[i], padded[j]): x = member i (columns), y = member j (rows)
-  PairSet ps{c.xinc.as<double>(), c.xinc.as<double>(), cnt * dim, cnt * dim, static_cast<int>(cnt),
-             static_cast<int>(cnt), static_cast<int>(dim)};
+  PairSet ps{c.xinc.as<double>(), c.xinc.as<double>(), len * ld, len * ld, static_cast<int>(cnt),
+             static_cast<int>(cnt), static_cast<int>(dim), static_cast<int>(ld)};
   std::vector<int> ords, conv;
   if (adaptive) {
     SK_CUDA(c.sqn.ensure(m * sizeof(double)));
-    SK_CUDA(launch_max_sqnorm(ps.d_xinc, m, cnt, dim, c.sqn.as<double>(), c.stream()));
+    SK_CUDA(launch_max_sqnorm(ps.d_xinc, m, cnt, dim, ld, c.sqn.as<double>(), c.stream()));
     ++c.aux_launches;
     std::vector<double> h(m);
     SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, m * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));

@@ -10,17 +10,17 @@
 // total = sum c = K at the tile's far corner.
 //
 // The register kernels carry the series in FACTORIAL-SCALED form
-// q[m] = m! alpha[m], r[m] = m! beta[m].  With p[m] = delta^m / m! and
-// pw[m] = delta^m the map becomes (exact algebra; only the rounding order
-// differs from the reference):
-//     q'[a] = sum_{b=0..a} q[a-b] p[b]          + pw[a] * sum_{k=1..N-a} r[k] / (a+k)!
-//     r'[b] = sum_{a=0..b-1} r[b-a] p[a]        + pw[b] * sum_{k=0..N-b} q[k] / (b+k)!
+// q[m] = m! alpha[m], r[m] = m! beta[m].  With p[m] = delta^m / m! the map
+// becomes (exact algebra; only the rounding order differs from the
+// reference):
+//     q'[a] = sum_{b=0..a} q[a-b] p[b]    + p[a] * sum_{k=1..N-a} r[k] a!/(a+k)!
+//     r'[b] = sum_{a=0..b-1} r[b-a] p[a]  + p[b] * sum_{k=0..N-b} q[k] b!/(b+k)!
 //     total = sum_a q'[a] / a!
 // i.e. two triangular Toeplitz products (the convolutions with p) and two
-// triangular Hankel products with constant 1/k! weights: ~2 (N+1)^2 DFMA per
-// tile instead of the literal 3 (N+1)^2 FP64 instructions.  The diagonal entry
-// a = b always takes alpha[0] (q[0]), never beta[0], as the reference's
-// `i >= j` branch does.
+// triangular Hankel products with constant weights: ~2 (N+1)^2 FP64 ops per
+// tile instead of the literal 3 (N+1)^2.  The diagonal entry a = b always
+// takes alpha[0] (q[0]), never beta[0], as the reference's `i >= j` branch
+// does.
 #pragma once
 
 #include <cstdint>
@@ -61,54 +61,75 @@ __device__ __forceinline__ double exact_dot(const double (&a)[DP], const double 
   return acc;
 }
 
-// Register tile step on scaled series (see header comment).  Returns total.
-// `fault` flips the sign of the W[1][1] contribution (the reference's
-// negative-control hook, tile_series.cpp:51-52).
+// 1/m as a compile-time-indexed constant (1 for m = 1, so no multiply).
+// Only these N+1 reciprocals appear as multipliers in the register solver:
+// few enough that ptxas keeps them in uniform registers, so every DFMA that
+// uses one reads just two vector register pairs (full FP64 issue rate).
+// Register tile step on factorial-scaled series (N <= kMaxRegOrder).
+//
+// With p[m] = delta^m / m!, ph[m] = delta^m / N! and the integer-weighted
+// Hankel sums
+//   U_b = sum_{k=0..N-b} q[k] N!/(b+k)!  = (N!/b!) sum_k q[k] b!/(b+k)!
+//   V_a = sum_{k=1..N-a} r[k] N!/(a+k)!  = (N!/a!) sum_k r[k] a!/(a+k)!
+// the map of the header comment becomes
+//   q'[a] = sum_{b<=a} q[a-b] p[b]  + ph[a] V_a
+//   r'[b] = sum_{a<b}  r[b-a] p[a]  + ph[b] U_b       (r'[0] = ph[0] U_0)
+//   total = (1/N!) sum_a q'[a] N!/a!
+// U, V and the total are Horner recurrences whose multipliers are the small
+// integers b+1, ..., N: DFMA immediates.
+//
+// Why: on B200 a DFMA that reads three distinct 64-bit vector registers
+// issues at 2/3 of the FP64 rate (register-file bank reads; measured,
+// profiles/fp64_operands_r01.txt), while one with an immediate (or
+// uniform / constant-bank) operand issues at the full rate.  Only the two
+// convolutions and the final combine (80 of the 170 FP64 operations at
+// N = 8) still need three vector operands.  Returns total.  `fault` flips
+// the sign of the W[1][1] contribution (the reference's negative-control
+// hook, tile_series.cpp:51-52).
 template <int N>
-__device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], const double (&r)[N + 1],
-                                                   double delta, double (&qo)[N + 1], double (&ro)[N + 1],
-                                                   bool fault) {
+__device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
+                                                   double (&qo)[N + 1], double (&ro)[N + 1], bool fault) {
   constexpr int n = N + 1;
-  double pw[n], p[n];
-  pw[0] = 1.0;
+  // ph[m] = delta^m / N!, p[m] = delta^m / m! = ph[m] * (N!/m!)
+  double ph[n], p[n];
+  ph[0] = c_inv_fact[N];
   p[0] = 1.0;
-  if constexpr (N >= 1) {
-    pw[1] = delta;
-    p[1] = delta;
+#pragma unroll
+  for (int m = 1; m < n; ++m) ph[m] = ph[m - 1] * delta;
+  if constexpr (N >= 1) p[1] = delta;
+#pragma unroll
+  for (int m = 2; m < n; ++m) p[m] = ph[m] * c_fact_ratio[N * (kMaxRegOrder + 1) + m];
+  // Hankel parts by integer Horner recurrences (immediate multipliers)
+  double u[n], v[N > 0 ? N : 1];
+#pragma unroll
+  for (int b = 0; b < n; ++b) {
+    double acc = q[0];
+#pragma unroll
+    for (int k = 1; k <= N - b; ++k) acc = fma(acc, static_cast<double>(b + k), q[k]);
+    u[b] = acc;
   }
 #pragma unroll
-  for (int m = 2; m < n; ++m) {
-    pw[m] = pw[m - 1] * delta;
-    p[m] = pw[m] * c_inv_fact[m];
+  for (int a = 0; a < N; ++a) {
+    double acc = r[1];
+#pragma unroll
+    for (int k = 2; k <= N - a; ++k) acc = fma(acc, static_cast<double>(a + k), r[k]);
+    v[a] = acc;
   }
-  // alpha' (row sums): Toeplitz(p) * q  +  diag(pw) * Hankel(1/k!) * r
+  // convolutions with p (p[0] = 1) + combine
 #pragma unroll
   for (int a = 0; a < n; ++a) {
     double acc = q[a];
 #pragma unroll
     for (int b = 1; b <= a; ++b) acc = fma(q[a - b], p[b], acc);
-    if (a < N) {
-      double s = r[1] * c_inv_fact[a + 1];
-#pragma unroll
-      for (int k = 2; k <= N - a; ++k) s = fma(r[k], c_inv_fact[a + k], s);
-      acc = (a == 0) ? acc + s : fma(pw[a], s, acc);
-    }
-    qo[a] = acc;
+    qo[a] = (a < N) ? fma(ph[a], v[a], acc) : acc;
   }
-  // beta' (column sums): Toeplitz(p) * r (strictly lower) + diag(pw) * Hankel(1/k!) * q
+  ro[0] = ph[0] * u[0];
 #pragma unroll
-  for (int b = 0; b < n; ++b) {
-    double t = (b <= 1) ? q[0] : q[0] * c_inv_fact[b];
+  for (int b = 1; b < n; ++b) {
+    double acc = r[b];
 #pragma unroll
-    for (int k = 1; k <= N - b; ++k) t = fma(q[k], c_inv_fact[b + k], t);
-    if (b == 0) {
-      ro[0] = t;
-    } else {
-      double acc = r[b];
-#pragma unroll
-      for (int a = 1; a < b; ++a) acc = fma(r[b - a], p[a], acc);
-      ro[b] = fma(pw[b], t, acc);
-    }
+    for (int a = 1; a < b; ++a) acc = fma(r[b - a], p[a], acc);
+    ro[b] = fma(ph[b], u[b], acc);
   }
   if constexpr (N >= 1) {
     if (fault) {
@@ -117,10 +138,11 @@ __device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], con
       ro[1] -= c11;
     }
   }
-  double total = qo[0];
+  // total = sum_a q'[a] / a! = (1/N!) * Horner(q'; multipliers 1..N)
+  double tot = qo[0];
 #pragma unroll
-  for (int a = 1; a < n; ++a) total = fma(qo[a], c_inv_fact[a], total);
-  return total;
+  for (int a = 1; a < n; ++a) tot = fma(tot, static_cast<double>(a), qo[a]);
+  return tot * c_inv_fact[N];
 }
 
 // Literal reference tile step (wavefront.cpp:35-59) on UNSCALED series with a
@@ -160,6 +182,43 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
 
 __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// v = *p on lanes where pred holds (predicated ld.shared, no branch).
+__device__ __forceinline__ void ld_shared_if(bool pred, const double* p, double& v) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
+      : "+d"(v)
+      : "r"(a), "r"(static_cast<unsigned>(pred)));
+}
+
+__device__ __forceinline__ void ld_shared2_if(bool pred, const double* p, double& v0, double& v1) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
+      : "+d"(v0), "+d"(v1)
+      : "r"(a), "r"(static_cast<unsigned>(pred)));
+}
+
+// Predicated global stores (no branch, keeps the step loop one basic block).
+__device__ __forceinline__ void st_global_if(bool pred, double* p, double v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
+      "r"(static_cast<unsigned>(pred))
+      : "memory");
+}
+__device__ __forceinline__ void st_global_cg2_if(bool pred, double* p, double v0, double v1) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.global.cg.v2.f64 [%0], {%1, %2};\n\t}" ::"l"(p),
+      "d"(v0), "d"(v1), "r"(static_cast<unsigned>(pred))
+      : "memory");
+}
+__device__ __forceinline__ void st_release_gpu_if(bool pred, unsigned long long* p, unsigned long long v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.release.gpu.global.u64 [%0], %1;\n\t}" ::"l"(p),
+      "l"(v), "r"(static_cast<unsigned>(pred))
+      : "memory");
 }
 
 __device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {

@@ -21,16 +21,23 @@ inline int pick_dp(size_t dim) {
   return 0;
 }
 
-cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, double* out,
+// Device increment layout: per series `len` rows of `ld` doubles, row 0 zero,
+// row k+1 = dz_k zero-padded to ld (ld = pick_dp(d), or d on the table path).
+inline size_t inc_ld(size_t dim) {
+  const int dp = pick_dp(dim);
+  return dp > 0 ? static_cast<size_t>(dp) : dim;
+}
+cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, size_t ld, double* out,
                               cudaStream_t st);
-cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, double* out,
+cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, size_t ld, double* out,
                               cudaStream_t st);
 cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                                size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
-                               int dim, unsigned long long* out, cudaStream_t st);
+                               int dim, int ld, unsigned long long* out, cudaStream_t st);
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
-                             int bands, int dim, double* tab, unsigned long long tab_stride, cudaStream_t st);
+                             int bands, int dim, int ld, double* tab, unsigned long long tab_stride,
+                             cudaStream_t st);
 cudaError_t launch_grid_init(double* grid, size_t nout, size_t lx, size_t ly, cudaStream_t st);
 cudaError_t launch_step_tile_literal(double delta, int order, const double* w65, const double* in, double* out,
                                      cudaStream_t st);
@@ -38,7 +45,11 @@ cudaError_t launch_step_tile_fast(double delta, int order, const double* in, dou
 
 // Sweep instantiations: one TU per register order N in 1..16 and N = 0
 // (literal arithmetic, runtime order up to 64).
-cudaError_t sweep_launch(int n_template, int dp, int grid, cudaStream_t stream, const SweepParams& P);
-cudaError_t sweep_occupancy(int n_template, int dp, int* blocks_per_sm);
+// exact: reference-identical delta (sequential non-FMA dot) + per-pair
+// max|delta| tracking; otherwise an FMA dot and no max tracking.
+// extras: knot grid / diagonal outputs.
+cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, int grid, cudaStream_t stream,
+                         const SweepParams& P);
+cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, int* blocks_per_sm);
 
 }  // namespace skb

@@ -1,5 +1,5 @@
 // One translation unit per truncation order: compiled once per SK_N value
-// (Makefile) so the 17 x 5 sweep instantiations build in parallel.
+// (Makefile) so the 17 x 5 x 2 sweep instantiations build in parallel.
 #include <cuda_runtime.h>
 
 #include "sk_sweep.cuh"
@@ -10,52 +10,67 @@
 
 namespace skb {
 
-template <int N, int DP>
+template <int N, int DP, bool EXACT, bool EXTRAS>
+static size_t smem_bytes() {
+  return static_cast<size_t>(kSweepWarps) * stage_doubles_per_warp(N, DP) * sizeof(double);
+}
+
+template <int N, int DP, bool EXACT, bool EXTRAS>
+static cudaError_t prepare() {
+  const size_t smem = smem_bytes<N, DP, EXACT, EXTRAS>();
+  if (smem > 48 * 1024)
+    return cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem));
+  return cudaSuccess;
+}
+
+template <int N, int DP, bool EXACT, bool EXTRAS>
 static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& P) {
-  const size_t smem = static_cast<size_t>(kSweepWarps) * stage_doubles_per_warp<N>() * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  sweep_kernel<N, DP><<<grid, kSweepWarps * 32, smem, stream>>>(P);
+  cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
+  if (e != cudaSuccess) return e;
+  sweep_kernel<N, DP, EXACT, EXTRAS><<<grid, kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>(), stream>>>(P);
   return cudaGetLastError();
 }
 
-template <int N, int DP>
+template <int N, int DP, bool EXACT, bool EXTRAS>
 static cudaError_t occupancy_one(int* blocks_per_sm) {
-  const size_t smem = static_cast<size_t>(kSweepWarps) * stage_doubles_per_warp<N>() * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<N, DP>, kSweepWarps * 32, smem);
+  cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<N, DP, EXACT, EXTRAS>,
+                                                       kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>());
 }
 
 #define SK_CAT2(a, b) a##b
 #define SK_CAT(a, b) SK_CAT2(a, b)
 
-cudaError_t SK_CAT(sweep_launch_n, SK_N)(int dp, int grid, cudaStream_t stream, const SweepParams& P) {
-  switch (dp) {
-    case 0: return launch_one<SK_N, 0>(grid, stream, P);
-    case 2: return launch_one<SK_N, 2>(grid, stream, P);
-    case 4: return launch_one<SK_N, 4>(grid, stream, P);
-    case 8: return launch_one<SK_N, 8>(grid, stream, P);
-    case 16: return launch_one<SK_N, 16>(grid, stream, P);
-    default: return cudaErrorInvalidValue;
+// Variants: N > 0 -> (exact, extras) in {(0,0), (1,0), (0,1)}; (1,1) maps to
+// (1,0) + ... never requested (grids never ask for max|rho|).  N = 0 (literal
+// kernel) always runs the fully general <true, true> variant.
+#if SK_N > 0
+#define SK_VAR(FN, DPV, ...)                                                      \
+  (extras ? FN<SK_N, DPV, false, true>(__VA_ARGS__)                               \
+          : (exact ? FN<SK_N, DPV, true, false>(__VA_ARGS__) : FN<SK_N, DPV, false, false>(__VA_ARGS__)))
+#else
+#define SK_VAR(FN, DPV, ...) FN<SK_N, DPV, true, true>(__VA_ARGS__)
+#endif
+
+#define SK_DP_SWITCH(FN, ...)                    \
+  switch (dp) {                                  \
+    case 0: return SK_VAR(FN, 0, __VA_ARGS__);   \
+    case 2: return SK_VAR(FN, 2, __VA_ARGS__);   \
+    case 4: return SK_VAR(FN, 4, __VA_ARGS__);   \
+    case 8: return SK_VAR(FN, 8, __VA_ARGS__);   \
+    case 16: return SK_VAR(FN, 16, __VA_ARGS__); \
+    default: return cudaErrorInvalidValue;       \
   }
+
+cudaError_t SK_CAT(sweep_launch_n, SK_N)(int dp, bool exact, bool extras, int grid, cudaStream_t stream,
+                                         const SweepParams& P) {
+  SK_DP_SWITCH(launch_one, grid, stream, P)
 }
 
-cudaError_t SK_CAT(sweep_occupancy_n, SK_N)(int dp, int* blocks_per_sm) {
-  switch (dp) {
-    case 0: return occupancy_one<SK_N, 0>(blocks_per_sm);
-    case 2: return occupancy_one<SK_N, 2>(blocks_per_sm);
-    case 4: return occupancy_one<SK_N, 4>(blocks_per_sm);
-    case 8: return occupancy_one<SK_N, 8>(blocks_per_sm);
-    case 16: return occupancy_one<SK_N, 16>(blocks_per_sm);
-    default: return cudaErrorInvalidValue;
-  }
+cudaError_t SK_CAT(sweep_occupancy_n, SK_N)(int dp, bool exact, bool extras, int* blocks_per_sm) {
+  SK_DP_SWITCH(occupancy_one, blocks_per_sm)
 }
 
 }  // namespace skb
