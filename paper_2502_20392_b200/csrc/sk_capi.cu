@@ -178,7 +178,7 @@ struct Ctx {
   cudaStream_t user = nullptr;
   int sms = 148;
   DevBuf raw_x, raw_y, xinc, yinc, sqn, pairs, values, err, maxr, prog, queue, abuf, tab, grid, diag, w65, tile_io,
-      scan;
+      scan, wd;
   bool stats_on = false;
   std::vector<StatRec> stats;
   uint64_t sweep_launches = 0, aux_launches = 0;
@@ -191,7 +191,7 @@ struct Ctx {
       cudaEventDestroy(r.b);
     }
     DevBuf* all[] = {&raw_x, &raw_y, &xinc, &yinc, &sqn, &pairs, &values, &err, &maxr,
-                     &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan};
+                     &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan, &wd};
     for (DevBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
   }
@@ -272,6 +272,27 @@ int record_end(Ctx& c, StatRec* rec, sk_status* st) {
   return SK_OK;
 }
 
+// Dependency-wait watchdog (SK_WATCHDOG_S, default 60 s): a sweep whose
+// inter-band wait exceeds it aborts and reports instead of hanging the GPU.
+unsigned long long watchdog_ns() {
+  static const unsigned long long ns = [] {
+    const char* e = std::getenv("SK_WATCHDOG_S");
+    const double s = e ? std::atof(e) : 60.0;
+    return static_cast<unsigned long long>((s > 0 ? s : 60.0) * 1e9);
+  }();
+  return ns;
+}
+
+int check_watchdog(Ctx& c, sk_status* st) {
+  unsigned long long h[5] = {0, 0, 0, 0, 0};
+  SK_CUDA(cudaMemcpyAsync(h, c.wd.p, sizeof h, cudaMemcpyDeviceToHost, c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  if (h[0] == 0) return SK_OK;
+  return set_status(st, SK_INTERNAL, 0, 0,
+                    "sweep watchdog: dependency wait timed out (pair %llu band %llu needs %llu, saw %llu)", h[1], h[2],
+                    h[3], h[4]);
+}
+
 // One persistent sweep launch per (order, pair chunk).  px/py/pout are
 // launch-local pair lists of equal length.
 int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const std::vector<uint32_t>& py,
@@ -332,6 +353,8 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     SK_CUDA(cudaMemsetAsync(c.prog.p, 0, slots * bands * sizeof(unsigned long long), c.stream()));
     SK_CUDA(c.queue.ensure(sizeof(unsigned)));
     SK_CUDA(cudaMemsetAsync(c.queue.p, 0, sizeof(unsigned), c.stream()));
+    SK_CUDA(c.wd.ensure(8 * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemsetAsync(c.wd.p, 0, 8 * sizeof(unsigned long long), c.stream()));
     if (bands > 1) SK_CUDA(c.abuf.ensure(slots * col_bytes));
     if (dp == 0) {
       SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
@@ -362,6 +385,8 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.abuf = bands > 1 ? c.abuf.as<double>() : nullptr;
     P.prog = c.prog.as<unsigned long long>();
     P.queue = c.queue.as<unsigned>();
+    P.watchdog = c.wd.as<unsigned long long>();
+    P.watchdog_ns = watchdog_ns();
     P.values = o.d_values;
     P.err = o.d_err;
     P.maxrho = o.d_maxrho;
@@ -377,6 +402,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     SK_CUDA(sweep_launch(ntempl, dp, exact, extras, blocks, c.stream(), P));
     if (int rc = record_end(c, &rec, st)) return rc;
     ++c.sweep_launches;
+    if (int rc = check_watchdog(c, st)) return rc;
   }
   return SK_OK;
 }

@@ -65,6 +65,15 @@ __device__ __forceinline__ double exact_dot(const double (&a)[DP], const double 
 // Only these N+1 reciprocals appear as multipliers in the register solver:
 // few enough that ptxas keeps them in uniform registers, so every DFMA that
 // uses one reads just two vector register pairs (full FP64 issue rate).
+// N!/m! as a compile-time double (an exact integer below 2^53 for N <= 16:
+// DFMA/DMUL immediate or uniform constant).
+template <int N>
+__host__ __device__ constexpr double kFactRatio(int m) {
+  double r = 1.0;
+  for (int k = m + 1; k <= N; ++k) r *= static_cast<double>(k);
+  return r;
+}
+
 // Register tile step on factorial-scaled series (N <= kMaxRegOrder).
 //
 // With p[m] = delta^m / m!, ph[m] = delta^m / N! and the integer-weighted
@@ -90,15 +99,28 @@ template <int N>
 __device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
                                                    double (&qo)[N + 1], double (&ro)[N + 1], bool fault) {
   constexpr int n = N + 1;
-  // ph[m] = delta^m / N!, p[m] = delta^m / m! = ph[m] * (N!/m!)
+  // ph[m] = delta^m / N! by a depth-4 product tree (d2 = delta^2, d4 = delta^4);
+  // p[m] = delta^m / m! = ph[m] * (N!/m!), an integer immediate multiplier
   double ph[n], p[n];
   ph[0] = c_inv_fact[N];
   p[0] = 1.0;
+  if constexpr (N >= 1) {
+    const double d2 = delta * delta;
+    const double d4 = d2 * d2;
+    ph[1] = ph[0] * delta;
 #pragma unroll
-  for (int m = 1; m < n; ++m) ph[m] = ph[m - 1] * delta;
-  if constexpr (N >= 1) p[1] = delta;
+    for (int m = 2; m < n; ++m) {
+      if (m < 4)
+        ph[m] = ph[m - 2] * d2;
+      else if (m < 8)
+        ph[m] = ph[m - 4] * d4;
+      else
+        ph[m] = ph[m - 8] * (d4 * d4);
+    }
+    p[1] = delta;
 #pragma unroll
-  for (int m = 2; m < n; ++m) p[m] = ph[m] * c_fact_ratio[N * (kMaxRegOrder + 1) + m];
+    for (int m = 2; m < n; ++m) p[m] = ph[m] * kFactRatio<N>(m);
+  }
   // Hankel parts by integer Horner recurrences (immediate multipliers)
   double u[n], v[N > 0 ? N : 1];
 #pragma unroll
@@ -115,22 +137,24 @@ __device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], con
     for (int k = 2; k <= N - a; ++k) acc = fma(acc, static_cast<double>(a + k), r[k]);
     v[a] = acc;
   }
-  // convolutions with p (p[0] = 1) + combine
+  // convolutions with p (p[0] = 1), in lockstep over the shared multiplier
+  // p[b] so consecutive DFMAs can reuse it, then the combine
 #pragma unroll
-  for (int a = 0; a < n; ++a) {
-    double acc = q[a];
+  for (int a = 0; a < n; ++a) qo[a] = q[a];
 #pragma unroll
-    for (int b = 1; b <= a; ++b) acc = fma(q[a - b], p[b], acc);
-    qo[a] = (a < N) ? fma(ph[a], v[a], acc) : acc;
-  }
-  ro[0] = ph[0] * u[0];
+  for (int c = 1; c < n; ++c) ro[c] = r[c];
 #pragma unroll
   for (int b = 1; b < n; ++b) {
-    double acc = r[b];
 #pragma unroll
-    for (int a = 1; a < b; ++a) acc = fma(r[b - a], p[a], acc);
-    ro[b] = fma(ph[b], u[b], acc);
+    for (int a = b; a < n; ++a) qo[a] = fma(q[a - b], p[b], qo[a]);
+#pragma unroll
+    for (int c = b + 1; c < n; ++c) ro[c] = fma(r[c - b], p[b], ro[c]);
   }
+#pragma unroll
+  for (int a = 0; a < N; ++a) qo[a] = fma(ph[a], v[a], qo[a]);
+  ro[0] = ph[0] * u[0];
+#pragma unroll
+  for (int b = 1; b < n; ++b) ro[b] = fma(ph[b], u[b], ro[b]);
   if constexpr (N >= 1) {
     if (fault) {
       const double c11 = 2.0 * q[0] * delta;
@@ -138,10 +162,17 @@ __device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], con
       ro[1] -= c11;
     }
   }
-  // total = sum_a q'[a] / a! = (1/N!) * Horner(q'; multipliers 1..N)
-  double tot = qo[0];
+  // total = sum_a q'[a] / a! = (1/N!) sum_a q'[a] (N!/a!): two interleaved
+  // accumulators with integer immediate weights (short dependency chains)
+  double te = qo[N], to = 0.0;
 #pragma unroll
-  for (int a = 1; a < n; ++a) tot = fma(tot, static_cast<double>(a), qo[a]);
+  for (int a = N - 1; a >= 0; --a) {
+    if (((N - a) & 1) == 0)
+      te = fma(qo[a], kFactRatio<N>(a), te);
+    else
+      to = (a == N - 1) ? qo[a] * kFactRatio<N>(a) : fma(qo[a], kFactRatio<N>(a), to);
+  }
+  const double tot = te + to;
   return tot * c_inv_fact[N];
 }
 
@@ -177,6 +208,12 @@ __device__ __forceinline__ double tile_step_literal(int order, const double* alp
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 

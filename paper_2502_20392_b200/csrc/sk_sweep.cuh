@@ -10,16 +10,18 @@
 // a skewed anti-diagonal of the band:
 //   * beta (left-edge series) of row i stays in lane t's REGISTERS from one
 //     column to the next;
-//   * alpha (bottom-edge series) moves one lane up per step by one rotation
-//     shuffle; lane 31, whose alpha' has just been handed to the band above,
-//     carries lane 0's input (the band-below alpha of column s) into it;
+//   * alpha (bottom-edge series) moves one lane up per step through a
+//     per-warp shared-memory slot array (lane t reads slot t-1, writes slot
+//     t); lane 0 reads the band below's alpha, lane 31 writes into a chunk
+//     buffer that the warp hands to the band above once per chunk;
 //   * the band-below alpha arrives through a per-pair column buffer in
 //     global memory (L2-resident), published every kPublish columns with
-//     st.release and staged kChunk columns ahead into shared memory with
+//     a fence + st.release and staged one chunk ahead into shared memory with
 //     ld.acquire + cp.async;
 //   * the column increments dx_j stream through a per-warp shared-memory ring
-//     (cp.async, one chunk ahead, bank-conflict-free padded rows); dy_i stays
-//     in registers.
+//     (cp.async, one chunk ahead, bank-conflict-free padded rows); the
+//     increment products of a whole chunk are contracted up front (16
+//     independent dots per lane) into shared memory.
 // No grid-wide barrier and no launch per diagonal exists: dependencies are
 // point-to-point progress counters, and every warp of a persistent grid pulls
 // units from one atomic queue in an order (group, band, pair-in-group) fixed
@@ -65,6 +67,8 @@ struct SweepParams {
   double* abuf;                   // slots x cols x NP
   unsigned long long* prog;       // slots x bands progress counters
   unsigned* queue;                // unit counter
+  unsigned long long* watchdog;   // [0] abort flag, [1..4] first stuck wait (p, b, need, seen)
+  unsigned long long watchdog_ns; // give up a dependency wait after this long
   double* values;                 // per output slot: K(1,1)
   unsigned long long* err;        // per output slot: min error key (init ~0)
   unsigned long long* maxrho;     // per output slot: max |delta| bits (init 0) or null
@@ -81,23 +85,91 @@ __host__ __device__ constexpr int col_stride(int N) { return (series_len(N) + 1)
 // dx ring row stride in doubles: 16-byte rows padded so that the 8 lanes of
 // an LDS.128 phase (columns j, j-1, ..., j-7) hit distinct bank groups.
 __host__ __device__ constexpr int ring_stride(int DP) { return DP <= 2 ? 2 : DP + 2; }
-// per warp: alpha stage (2 groups) | dx ring (DP > 0) | delta stage
-// (1 group computed in place for DP > 0, 2 groups copied from the table for DP = 0)
+// per warp: band-below alpha stage (2 groups) | lane-to-lane alpha slots (2 x 32)
+// | lane 31's outputs of the chunk | dx ring (DP > 0) | delta stage (1 group
+// computed in place for DP > 0, 2 groups copied from the table for DP = 0)
 __host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP) {
-  return 2 * kChunk * col_stride(N) + (DP > 0 ? kRing * ring_stride(DP) + kChunk * 32 : 2 * kChunk * 32);
+  return 2 * kChunk * col_stride(N) + 2 * 32 * col_stride(N) + kChunk * col_stride(N) +
+         (DP > 0 ? kRing * ring_stride(DP) + kChunk * 32 : 2 * kChunk * 32);
 }
 
-__device__ __forceinline__ void wait_progress(const unsigned long long* ptr, unsigned long long need,
-                                              unsigned long long& seen) {
-  // every lane polls the same word (one transaction); acquire orders the
-  // lane's later loads of the column buffer after the producer's release.
-  if (seen >= need) return;
-  unsigned long long v = ld_acquire_gpu(ptr);
-  while (v < need) {
-    __nanosleep(64);
-    v = ld_acquire_gpu(ptr);
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Dependency wait with a watchdog: a wait that exceeds P.watchdog_ns (a
+// scheduling bug -- by construction every awaited unit is running) records
+// itself, raises the abort flag and returns false instead of hanging the GPU;
+// every other waiting warp then bails out too.
+static __device__ __noinline__ bool wait_progress_slow(const unsigned long long* ptr, unsigned long long need,
+                                                       unsigned long long& seen, unsigned long long* wd,
+                                                       unsigned long long limit_ns, unsigned p, unsigned b) {
+  // poll with relaxed loads (no L1 invalidation per poll) and a growing
+  // back-off; the acquire is taken once the value is there
+  const unsigned long long t0 = globaltimer_ns();
+  unsigned ns = 32;
+  for (unsigned it = 1;; ++it) {
+    __nanosleep(ns);
+    if (ns < 1024) ns += ns >> 1;
+    if (ld_relaxed_gpu(ptr) >= need) break;
+    if ((it & 15) == 0) {
+      if (*reinterpret_cast<volatile unsigned long long*>(wd) != 0) return false;
+      if (globaltimer_ns() - t0 > limit_ns) {
+        if ((threadIdx.x & 31) == 0 && atomicCAS(wd, 0ull, 1ull) == 0ull) {
+          wd[1] = p;
+          wd[2] = b;
+          wd[3] = need;
+          wd[4] = ld_relaxed_gpu(ptr);
+        }
+        return false;
+      }
+    }
   }
-  seen = v;
+  seen = ld_acquire_gpu(ptr);
+  return true;
+}
+
+__device__ __forceinline__ bool wait_progress(const SweepParams& P, const unsigned long long* ptr,
+                                              unsigned long long need, unsigned long long& seen, unsigned p,
+                                              unsigned b) {
+  if (seen >= need) return true;
+  const unsigned long long v = ld_acquire_gpu(ptr);  // every lane polls the same word
+  if (v >= need) {
+    seen = v;
+    return true;
+  }
+  return wait_progress_slow(ptr, need, seen, P.watchdog, P.watchdog_ns, p, b);
+}
+
+template <int NA>
+__device__ __forceinline__ void lds_series(const double* src, double (&v)[NA], int n) {
+#pragma unroll
+  for (int m = 0; m < NA; m += 2) {
+    if (m + 1 < NA) {
+      if (NA <= kMaxRegOrder + 1 || m < n) {
+        const double2 t = *reinterpret_cast<const double2*>(src + m);
+        v[m] = t.x;
+        v[m + 1] = t.y;
+      }
+    } else if (NA <= kMaxRegOrder + 1 || m < n) {
+      v[m] = src[m];
+    }
+  }
+}
+
+template <int NA>
+__device__ __forceinline__ void sts_series(double* dst, const double (&v)[NA], int n) {
+#pragma unroll
+  for (int m = 0; m < NA; m += 2) {
+    if (NA <= kMaxRegOrder + 1 || m < n) {
+      double2 t;
+      t.x = v[m];
+      t.y = (m + 1 < NA) ? v[m + 1] : 0.0;
+      *reinterpret_cast<double2*>(dst + m) = t;
+    }
+  }
 }
 
 // N > 0: register kernel on factorial-scaled series.  N == 0: literal
@@ -113,15 +185,18 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   constexpr int NP = col_stride(N);
   constexpr int XS = ring_stride(DP);
   constexpr int kStage = kChunk * NP;
-  double* s_alpha = smem;                                         // 2 x kChunk x NP
-  double* s_ring = smem + 2 * kStage;                             // kRing x XS (DP > 0)
-  double* s_delta = s_ring + (DP > 0 ? kRing * XS : 0);           // kChunk x 32 (x2 for DP = 0)
+  double* s_alpha = smem;                                   // 2 x kChunk x NP
+  double* s_pass = s_alpha + 2 * kStage;                    // 2 x 32 x NP (step parity)
+  double* s_out = s_pass + 64 * NP;                         // kChunk x NP
+  double* s_ring = s_out + kStage;                          // kRing x XS (DP > 0)
+  double* s_delta = s_ring + (DP > 0 ? kRing * XS : 0);     // kChunk x 32 (x2 for DP = 0)
   const int n = N > 0 ? N + 1 : P.order + 1;
   const int rows = P.rows, cols = P.cols;
   const int row0 = static_cast<int>(b) * 32;
   const int rb = min(32, rows - row0);
   const int i = row0 + lane;
   const bool row_ok = lane < rb;
+  const bool last_row = row_ok && i == rows - 1;
   const unsigned slot = p % static_cast<unsigned>(P.slots);
   const unsigned long long base = static_cast<unsigned long long>(p) * static_cast<unsigned long long>(cols + 1);
   double* colbuf = P.abuf + static_cast<size_t>(slot) * static_cast<size_t>(cols) * NP;
@@ -136,44 +211,31 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   // band of the slot's previous pair (p - slots) reads.
   if (b == 0 && has_above && p >= static_cast<unsigned>(P.slots)) {
     unsigned long long seen0 = 0;
-    wait_progress(prog_row + (P.bands - 1),
-                  static_cast<unsigned long long>(p - P.slots) * (cols + 1) + cols, seen0);
+    if (!wait_progress(P, prog_row + (P.bands - 1),
+                       static_cast<unsigned long long>(p - P.slots) * (cols + 1) + cols, seen0, p, b))
+      return;
   }
 
-  // Row increment (register resident for the whole band); increments are
-  // stored with row stride DP behind one leading zero row.
-  double dy[DP > 0 ? DP : 1];
+  // increments are stored with row stride DP behind one leading zero row
+  const double* yrow = nullptr;
   const double* xser = nullptr;
   const double* tab = nullptr;
   if constexpr (DP > 0) {
-    const double* yrow = P.yinc + P.pair_y[p] * P.sy + static_cast<size_t>(row_ok ? i + 1 : 0) * DP;
-#pragma unroll
-    for (int c = 0; c < DP; c += 2) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(yrow + c));
-      dy[c] = v.x;
-      dy[c + 1] = v.y;
-    }
+    yrow = P.yinc + P.pair_y[p] * P.sy + static_cast<size_t>(row_ok ? i + 1 : 0) * DP;
     xser = P.xinc + P.pair_x[p] * P.sx + DP;  // row j of the pair at xser + j * DP
   } else {
     tab = P.rho_tab + static_cast<size_t>(p) * P.tab_stride + static_cast<size_t>(b) * (cols + 31) * 32;
-    dy[0] = 0.0;
   }
 
-  // Loop-carried state, ping-ponged between the A and B sets so the
-  // (unrolled-by-2) step loop needs no register copies:
-  //   qo*: this lane's alpha' (lane 31: the feed for lane 0)
-  //   ro*: this lane's beta' = beta of the next column of its row.
-  // Before a lane's first column (j < 0) it runs the delta = 0 tile on unit
-  // series, whose output is the unit series again, so beta is e0 exactly at
-  // j = 0 without a select.
-  double qoA[NA], roA[NA], qoB[NA], roB[NA];
+  // Loop-carried register state: this lane's beta (the left edge of its next
+  // tile).  Before a lane's first column (j < 0) it runs the delta = 0 tile
+  // on unit series, whose output is the unit series again, so beta is e0
+  // exactly at j = 0 without a select (the alpha slots start at e0 too).
+  double roA[NA], roB[NA];
 #pragma unroll
-  for (int m = 0; m < NA; ++m) {
-    qoA[m] = (m == 0) ? 1.0 : 0.0;
-    roA[m] = (m == 0) ? 1.0 : 0.0;
-  }
+  for (int m = 0; m < NA; ++m) roA[m] = (m == 0) ? 1.0 : 0.0;
   double mx = 0.0;
-  unsigned long long errkey = ~0ull;
+  unsigned jkey = ~0u;  // (first failing column << 2) | code for this lane
   unsigned long long seen = 0;
   const int steps = cols + rb - 1;
 
@@ -209,70 +271,58 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     // band 0: the bottom edge of the domain is the unit series in every column
     for (int e = lane; e < 2 * kStage; e += 32) s_alpha[e] = (e % NP == 0) ? 1.0 : 0.0;
   }
+  for (int e = lane; e < 64 * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
   if constexpr (DP > 0) {
     // columns -32..-1 (ring rows 32..63): zero increments => delta = 0
     for (int e = lane; e < 32 * XS; e += 32) s_ring[32 * XS + e] = 0.0;
   }
   __syncwarp();
-  if (has_below) wait_progress(prog_row + (b - 1), base + min(cols, kChunk), seen);
+  if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, kChunk), seen, p, b)) return;
   stage_group(0);
 
-  const int src_lane = (lane + 31) & 31;
-  const bool feeder = lane == 31;
-  const double* xw = s_ring;
+  // step s writes slot [s & 1][lane] and reads [(s - 1) & 1][lane - 1]: the
+  // double buffer needs only one __syncwarp per step (RAW); the WAR reuse
+  // two steps later is ordered by the intervening one
+  double* const my_pass = s_pass + lane * NP;
+  const double* const below_pass = s_pass + (lane - 1) * NP;
 
-  // one tile step: column j = s - lane of row i (one basic block: all
-  // conditional work is predicated)
-  auto step = [&](int s, const double* stage_col, double delta, double (&qo_in)[NA], double (&r_in)[NA],
-                  double (&qo_out)[NA], double (&ro_out)[NA]) {
+  // one tile step: column j = s - lane of row i
+  auto step = [&](int s, int k, int par, const double* stage, double delta, double (&r_in)[NA],
+                  double (&ro_out)[NA]) {
     const int j = s - lane;
-    // lane 31's alpha' went to the band above at the end of the previous
-    // step; it now carries lane 0's input (predicated shared loads)
-#pragma unroll
-    for (int m = 0; m < NA; m += 2)
-      if (N > 0 || m < n) {
-        if (m + 1 < NA)
-          ld_shared2_if(feeder, stage_col + m, qo_in[m], qo_in[m + 1]);
-        else
-          ld_shared_if(feeder, stage_col + m, qo_in[m]);
-      }
-    double q[NA];
-#pragma unroll
-    for (int m = 0; m < NA; ++m)
-      if (N > 0 || m < n) q[m] = __shfl_sync(0xffffffffu, qo_in[m], src_lane);
+    double q[NA], qo[NA];
+    // alpha: lane 0 from the band below (stage), lane t from lane t-1's slot
+    lds_series<NA>(lane == 0 ? stage + k * NP : below_pass + (par ^ 1) * 32 * NP, q, n);
 
     double total;
     if constexpr (N > 0) {
-      total = tile_step_scaled<N>(q, r_in, delta, qo_out, ro_out, fault);
+      total = tile_step_scaled<N>(q, r_in, delta, qo, ro_out, fault);
     } else {
-      total = tile_step_literal(P.order, q, r_in, delta, P.w65, qo_out, ro_out);
+      total = tile_step_literal(P.order, q, r_in, delta, P.w65, qo, ro_out);
     }
+    // alpha' up: lane 31 parks it for the band above, the others in their slot
+    sts_series<NA>(lane == 31 ? s_out + k * NP : my_pass + par * 32 * NP, qo, n);
+    __syncwarp();
 
+#ifndef SK_EXPERIMENT_NO_CHECKS
     const bool active = row_ok && j >= 0 && j < cols;
-    const double ad = fabs(delta);
-    if constexpr (EXACT) mx = fmax(mx, active ? ad : 0.0);
-    // the reference's throw order inside a tile: delta guard, corner check,
-    // non-finite total (wavefront.cpp:150-173); first tile in (diagonal, row)
-    // order wins -> per-lane running min of the key, one atomic per band
-    const unsigned code = !(ad <= kDeltaOverflowLimit)                   ? kErrDelta
-                          : (strict && corner_mismatch(q[0], r_in[0]))   ? kErrCorner
-                          : !isfinite(total)                             ? kErrNonFinite
-                                                                         : 0u;
-    const unsigned long long key = err_key(i, j, code);
-    errkey = (active && code != 0u && key < errkey) ? key : errkey;
-    st_global_if(active && i == rows - 1 && j == cols - 1, P.values + out, total);
+    // the reference's throw order inside a tile: delta guard (checked when
+    // the chunk's deltas are formed), corner check, non-finite total
+    // (wavefront.cpp:150-173); the first failing tile of the lane wins
+    const unsigned code = (strict && corner_mismatch(q[0], r_in[0])) ? kErrCorner
+                          : !isfinite(total)                         ? kErrNonFinite
+                                                                     : 0u;
+    const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
+    jkey = (active && code != 0u && kk < jkey) ? kk : jkey;
+#else
+    const bool active = row_ok && j >= 0 && j < cols;
+#endif
+    st_global_if(last_row && j == cols - 1, P.values + out, total);
     if constexpr (EXTRAS) {
       if (P.grid)
         st_global_if(active, P.grid + out * P.grid_stride + static_cast<size_t>(j + 1) * (rows + 1) + (i + 1), total);
       if (P.diag) st_global_if(active && i == j, P.diag + out * P.diag_stride + i, total);
     }
-    // hand alpha' up to the band above (predicated, lane 31 only)
-    const bool hand = has_above && feeder && j >= 0 && j < cols;
-    double* dst = colbuf + static_cast<ptrdiff_t>(j) * NP;
-#pragma unroll
-    for (int m = 0; m < NA; m += 2)
-      if (N > 0 || m < n) st_global_cg2_if(hand, dst + m, qo_out[m], (m + 1 < NA) ? qo_out[m + 1] : 0.0);
-    st_release_gpu_if(hand && ((((j + 1) % kPublish) == 0) || j + 1 == cols), prog_row + b, base + j + 1);
   };
 
   const int ngroups_in = (cols + kChunk - 1) / kChunk;
@@ -280,7 +330,8 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   for (int c0 = 0, chunk = 0; c0 < steps; c0 += kChunk, ++chunk) {
     __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
     if (chunk + 1 < ngroups) {
-      if (has_below) wait_progress(prog_row + (b - 1), base + min(cols, (chunk + 2) * kChunk), seen);
+      if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, (chunk + 2) * kChunk), seen, p, b))
+        return;
       stage_group(chunk + 1);
       cp_async_wait<1>();
     } else {
@@ -288,53 +339,113 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     }
     __syncwarp();
     const double* stage = s_alpha + (chunk & 1) * kStage;
-    const double* dst = s_delta + (DP > 0 ? 0 : (chunk & 1) * kChunk * 32);
-    if constexpr (DP > 0) {
-      // the chunk's increment products: 16 independent dots per lane
-      // (lane t, step c0 + k -> column c0 + k - t), staged in shared memory
-#pragma unroll 4
-      for (int k = 0; k < kChunk; ++k) {
-        const double* xr = xw + ((c0 + k - lane) & (kRing - 1)) * XS;
-        double dx[DP];
+    const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * kChunk * 32);
+    const int kend = min(kChunk, steps - c0);
+    // the chunk's increment products (lane t, step c0 + k -> column c0 + k - t)
+    // with the delta guard (wavefront.cpp:150-155) and max|delta|
+    {
+      double dy[DP > 0 ? DP : 1];
+      if constexpr (DP > 0) {
 #pragma unroll
         for (int c = 0; c < DP; c += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(xr + c);
-          dx[c] = v.x;
-          dx[c + 1] = v.y;
+          const double2 v = __ldg(reinterpret_cast<const double2*>(yrow + c));
+          dy[c] = v.x;
+          dy[c + 1] = v.y;
         }
-        double dl;
-        if constexpr (EXACT) {
-          dl = exact_dot<DP>(dx, dy);
-        } else {
-          // pairwise-tree FMA dot (short dependency chain)
-          double acc[2] = {dx[0] * dy[0], dx[1] * dy[1]};
-#pragma unroll
-          for (int c = 2; c < DP; ++c) acc[c & 1] = fma(dx[c], dy[c], acc[c & 1]);
-          dl = acc[0] + acc[1];
-        }
-        s_delta[k * 32 + lane] = dl;
       }
-      __syncwarp();
+#pragma unroll 1
+      for (int k0 = 0; k0 < kChunk; k0 += 4) {
+        double dd[4];
+        if constexpr (DP > 0) {
+          // four columns at a time: all loads first, then four independent
+          // two-accumulator dots
+          double dx[4][DP];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double* xr = s_ring + ((c0 + k0 + u - lane) & (kRing - 1)) * XS;
+#pragma unroll
+            for (int c = 0; c < DP; c += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(xr + c);
+              dx[u][c] = v.x;
+              dx[u][c + 1] = v.y;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if constexpr (EXACT) {
+              dd[u] = exact_dot<DP>(dx[u], dy);
+            } else {
+              double e0 = dx[u][0] * dy[0], e1 = dx[u][1] * dy[1];
+#pragma unroll
+              for (int c = 2; c < DP; c += 2) {
+                e0 = fma(dx[u][c], dy[c], e0);
+                e1 = fma(dx[u][c + 1], dy[c + 1], e1);
+              }
+              dd[u] = e0 + e1;
+            }
+            s_delta[(k0 + u) * 32 + lane] = dd[u];
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dd[u] = dl[(k0 + u) * 32 + lane];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          const int j = c0 + k - lane;
+          const bool act = row_ok && j >= 0 && j < cols && k < kend;
+          const double ad = fabs(dd[u]);
+          if constexpr (EXACT) mx = fmax(mx, act ? ad : 0.0);
+          const unsigned kk = (static_cast<unsigned>(j) << 2) | kErrDelta;
+          jkey = (act && !(ad <= kDeltaOverflowLimit) && kk < jkey) ? kk : jkey;
+        }
+      }
     }
-    const int kend = min(kChunk, steps - c0);
+    __syncwarp();
     int k = 0;
 #pragma unroll 1
     for (; k + 1 < kend; k += 2) {
-      const double d0 = dst[k * 32 + lane];
-      const double d1 = dst[(k + 1) * 32 + lane];
-      step(c0 + k, stage + k * NP, d0, qoA, roA, qoB, roB);
-      step(c0 + k + 1, stage + (k + 1) * NP, d1, qoB, roB, qoA, roA);
+      const double d0 = dl[k * 32 + lane];
+      const double d1 = dl[(k + 1) * 32 + lane];
+      step(c0 + k, k, 0, stage, d0, roA, roB);
+      step(c0 + k + 1, k + 1, 1, stage, d1, roB, roA);
     }
     if (k < kend) {
-      step(c0 + k, stage + k * NP, dst[k * 32 + lane], qoA, roA, qoB, roB);
+      step(c0 + k, k, k & 1, stage, dl[k * 32 + lane], roA, roB);
 #pragma unroll
-      for (int m = 0; m < NA; ++m) {
-        qoA[m] = qoB[m];
-        roA[m] = roB[m];
+      for (int m = 0; m < NA; ++m) roA[m] = roB[m];
+    }
+    // hand lane 31's alpha' of this chunk (columns c0 - 31 .. c0 + kend - 32)
+    // to the band above, then publish progress every kPublish columns
+    if (has_above) {
+      const int jfirst = c0 - 31;
+      const int pieces = kend * NP / 2;
+      for (int e = lane; e < pieces; e += 32) {
+        const int kk = e / (NP / 2);
+        const int jj = jfirst + kk;
+        if (jj >= 0 && jj < cols) {
+          const double2 v = *reinterpret_cast<const double2*>(s_out + 2 * e);
+          __stcg(reinterpret_cast<double2*>(colbuf + static_cast<size_t>(jj) * NP + (2 * e - kk * NP)), v);
+        }
+      }
+      // columns handed up before / after this chunk
+      const int done0 = min(max(c0 - 31, 0), cols);
+      const int done1 = min(max(c0 + kend - 31, 0), cols);
+      if (done1 > done0 && (done1 == cols || done1 / kPublish != done0 / kPublish)) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(prog_row + b, base + done1);
       }
     }
   }
-  if (errkey != ~0ull) atomicMin(P.err + out, errkey);
+  if (!has_above && P.bands > 1) {
+    // the last band publishes completion too: the slot's next pair (p + slots)
+    // may only rewrite the column buffer once this band has read all of it
+    cp_async_wait<0>();
+    __syncwarp();
+    if (lane == 0) st_release_gpu(prog_row + b, base + cols);
+  }
+  if (jkey != ~0u) atomicMin(P.err + out, err_key(i, jkey >> 2, jkey & 3u));
   if constexpr (EXACT) {
     if (P.maxrho) {
 #pragma unroll
@@ -359,6 +470,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, SK_MIN_BLOCKS) sweep_kernel(
     if (lane == 0) u = atomicAdd(P.queue, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= total_units) return;
+    if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) return;
     // unit order: (group g, band b, pair q within the group)
     const unsigned g = u / gsz;
     const unsigned rem = u - g * gsz;
