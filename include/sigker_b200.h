@@ -127,6 +127,11 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
             double* pair_max, double* max_product, int* converged, sk_status* entry_status,
             sk_status* st);
 
+/* Row-major upper-triangle pair indices [first, last) that shard `shard` of
+ * `nshards` evaluates in sk_gram (equal pair counts; pairs cost the same
+ * because the family is padded to one length).  Host arithmetic only. */
+int sk_gram_shard_range(size_t m, size_t shard, size_t nshards, size_t* first, size_t* last);
+
 /* Device-time accounting of the sweep kernels on the calling thread
  * (CUDA events around every sweep launch). */
 typedef struct sk_stats {

@@ -27,7 +27,7 @@ SK_W_FAULT = 4
 EXPORTED = [
     "sk_abi_version", "sk_device_count", "sk_set_device", "sk_set_stream",
     "sk_propagate", "sk_max_abs_rho", "sk_estimate_order", "sk_step_tile",
-    "sk_step_tile_fast", "sk_pairwise", "sk_pairwise_device", "sk_gram",
+    "sk_step_tile_fast", "sk_pairwise", "sk_pairwise_device", "sk_gram", "sk_gram_shard_range",
     "sk_stats_enable", "sk_stats_reset", "sk_stats_get", "sk_release",
 ]
 
@@ -78,6 +78,7 @@ def load():
                                 ctypes.c_uint32, P, P, P, P, ST], ctypes.c_int),
         "sk_gram": ([P, SZ, SZ, SZ, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint32, ctypes.c_int,
                      SZ, SZ, P, P, P, P, P, P, ST], ctypes.c_int),
+        "sk_gram_shard_range": ([SZ, SZ, SZ, P, P], ctypes.c_int),
         "sk_stats_enable": ([ctypes.c_int], ctypes.c_int),
         "sk_stats_reset": ([], ctypes.c_int),
         "sk_stats_get": ([ctypes.POINTER(SkStats)], ctypes.c_int),

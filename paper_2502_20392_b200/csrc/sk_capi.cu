@@ -225,8 +225,13 @@ int get_ctx(Ctx** out, sk_status* st) {
         w[i * (kMaxOrder + 1) + j] = v;
         w[j * (kMaxOrder + 1) + i] = v;
       }
-    SK_CUDA(c->w65.ensure(w.size() * sizeof(double)));
+    // second copy with the negative-control flip of W[1][1] (tile_series.cpp:51-52)
+    std::vector<double> wf(w);
+    wf[1 * (kMaxOrder + 1) + 1] = -wf[1 * (kMaxOrder + 1) + 1];
+    SK_CUDA(c->w65.ensure(2 * w.size() * sizeof(double)));
     SK_CUDA(cudaMemcpy(c->w65.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    SK_CUDA(cudaMemcpy(c->w65.as<double>() + w.size(), wf.data(), w.size() * sizeof(double),
+                       cudaMemcpyHostToDevice));
     c->ready = true;
     t_ctx = std::move(c);
   }
@@ -341,6 +346,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
       if (slots > fit) slots = std::max<size_t>(fit, 1);
       if (group > slots) group = slots;
     }
+    // test hooks: force small groups / slot counts to exercise slot reuse
+    if (const char* e = std::getenv("SK_FORCE_GROUP")) group = std::max<size_t>(1, std::min<size_t>(group, std::atoi(e)));
+    if (const char* e = std::getenv("SK_FORCE_SLOTS"))
+      slots = std::max<size_t>(group, std::min<size_t>(slots, std::atoi(e)));
     // workspace
     SK_CUDA(c.pairs.ensure(3 * npairs * sizeof(uint32_t)));
     uint32_t* d_px = c.pairs.as<uint32_t>();
@@ -370,7 +379,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.pair_out = d_po;
     P.sx = ps.sx;
     P.sy = ps.sy;
-    P.w65 = c.w65.as<double>();
+    P.w65 = c.w65.as<double>() + ((flags & SK_W_FAULT) ? (kMaxOrder + 1) * (kMaxOrder + 1) : 0);
     P.rho_tab = dp == 0 ? c.tab.as<double>() : nullptr;
     P.tab_stride = tab_elems;
     P.dim = ps.dim;
@@ -815,8 +824,8 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
   Ctx* cp = nullptr;
   if (int rc = get_ctx(&cp, st)) return rc;
   Ctx& c = *cp;
-  const size_t total_pairs = m * (m + 1) / 2;
-  const size_t t0 = total_pairs * shard / nshards, t1 = total_pairs * (shard + 1) / nshards;
+  size_t t0 = 0, t1 = 0;
+  sk_gram_shard_range(m, shard, nshards, &t0, &t1);
   const size_t np = t1 - t0;
   for (size_t k = 0; k < m * m; ++k) {
     if (values) values[k] = std::numeric_limits<double>::quiet_NaN();
@@ -940,6 +949,14 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
   }
   if (max_product) *max_product = best;
   if (first_fatal >= 0) return decode_err(he[first_fatal], st, nullptr, nullptr, dim);
+  return SK_OK;
+}
+
+int sk_gram_shard_range(size_t m, size_t shard, size_t nshards, size_t* first, size_t* last) {
+  if (nshards < 1 || shard >= nshards) return SK_INVALID_ARGUMENT;
+  const size_t total = m * (m + 1) / 2;
+  *first = total * shard / nshards;
+  *last = total * (shard + 1) / nshards;
   return SK_OK;
 }
 
