@@ -140,6 +140,8 @@ typedef struct sk_stats {
   double sweep_ms;         /* summed device time of the sweep launches    */
   double tiles;            /* tile-updates processed by those launches    */
   double tile_flops;       /* algorithmic FP64 flops, sum of F(N,d) per tile */
+  uint64_t table_launches; /* rho-table builds (d > 16: DMMA GEMM)        */
+  double table_ms;         /* summed device time of those builds          */
 } sk_stats;
 
 int sk_stats_enable(int enable);

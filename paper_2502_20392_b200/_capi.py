@@ -40,7 +40,8 @@ class SkStatus(ctypes.Structure):
 class SkStats(ctypes.Structure):
     _fields_ = [("sweep_launches", ctypes.c_uint64), ("aux_launches", ctypes.c_uint64),
                 ("sweep_ms", ctypes.c_double), ("tiles", ctypes.c_double),
-                ("tile_flops", ctypes.c_double)]
+                ("tile_flops", ctypes.c_double), ("table_launches", ctypes.c_uint64),
+                ("table_ms", ctypes.c_double)]
 
 
 _lib = None

@@ -99,36 +99,113 @@ __global__ void maxrho_scan_kernel(const double* __restrict__ xinc, const double
     atomicMax(out + pr, static_cast<unsigned long long>(__double_as_longlong(best)));
 }
 
-// Skewed delta table for the large-d path: entry ((b*(cols+31) + s)*32 + t)
-// holds rho(i = 32b + t, j = s - t) (0 outside the pair), so the sweep's warp
-// reads 256 contiguous bytes per step.  Exact sequential dot.
-__global__ void rho_table_kernel(const double* __restrict__ xinc, const double* __restrict__ yinc,
-                                 const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
-                                 unsigned long long sx, unsigned long long sy, int rows, int cols, int bands,
-                                 int dim, int ld, double* __restrict__ tab, unsigned long long tab_stride) {
-  const int pr = blockIdx.y;
+// rho table for the large-d path (d > 16): rho[i][j] = <dy_i, dx_j>, row-major
+// rows x cols per pair; the sweep gathers its deltas from it.
+//
+// Exact variant: sequential non-FMA dot (bit-identical deltas, needed when
+// the caller asks for the exact max|rho|).  One thread per entry.
+__global__ void rho_table_exact_kernel(const double* __restrict__ xinc, const double* __restrict__ yinc,
+                                       const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                                       unsigned long long sx, unsigned long long sy, int rows, int cols, int dim,
+                                       int ld, double* __restrict__ tab, unsigned long long tab_stride) {
+  const int pr = blockIdx.z;
+  const int j = blockIdx.x * 32 + threadIdx.x;
+  const int i = blockIdx.y * 8 + threadIdx.y;
+  if (i >= rows || j >= cols) return;
+  const double* xr = xinc + px[pr] * sx + static_cast<size_t>(j + 1) * ld;
+  const double* yr = yinc + py[pr] * sy + static_cast<size_t>(i + 1) * ld;
+  double acc = __dmul_rn(__ldg(xr), __ldg(yr));
+  for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + c), __ldg(yr + c)));
+  tab[pr * tab_stride + static_cast<size_t>(i) * cols + j] = acc;
+}
+
+// Tensor-core variant: FP64 DMMA (mma.sync m8n8k4 f64) tiled GEMM,
+// rho = dY * dX^T.  CTA tile 64 x 64 (i x j), 4 warps of 32 x 32, k staged
+// through shared memory in chunks of 32 with cp.async double buffering.
+// Increments are zero-padded to ld (multiple of 4), so k-padding is exact.
+constexpr int kGT = 64;            // CTA tile edge
+constexpr int kGK = 32;            // k chunk
+constexpr int kGS = kGK + 4;       // smem row stride (doubles): conflict-free fragment loads
+constexpr int kGemmSmem = 2 * 2 * kGT * kGS * 8;
+
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) rho_gemm_kernel(const double* __restrict__ xinc,
+                                                       const double* __restrict__ yinc,
+                                                       const uint32_t* __restrict__ px,
+                                                       const uint32_t* __restrict__ py, unsigned long long sx,
+                                                       unsigned long long sy, int rows, int cols, int ld,
+                                                       double* __restrict__ tab, unsigned long long tab_stride) {
+  extern __shared__ __align__(16) double gsm[];  // [buf][A|B][kGT][kGS]
+  const int pr = blockIdx.z;
+  const int i0 = blockIdx.y * kGT, j0 = blockIdx.x * kGT;
+  const double* ys = yinc + py[pr] * sy + ld;  // row i at ys + i * ld
   const double* xs = xinc + px[pr] * sx + ld;
-  const double* ys = yinc + py[pr] * sy + ld;
-  double* t = tab + pr * tab_stride;
-  const size_t steps = static_cast<size_t>(cols) + 31;
-  const size_t total = static_cast<size_t>(bands) * steps * 32;
-  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int lane = static_cast<int>(e & 31);
-    const size_t bs = e >> 5;
-    const int b = static_cast<int>(bs / steps);
-    const int s = static_cast<int>(bs - static_cast<size_t>(b) * steps);
-    const int i = b * 32 + lane;
-    const int j = s - lane;
-    double v = 0.0;
-    if (i < rows && j >= 0 && j < cols) {
-      const double* xr = xs + static_cast<size_t>(j) * ld;
-      const double* yr = ys + static_cast<size_t>(i) * ld;
-      double acc = __dmul_rn(__ldg(xr), __ldg(yr));
-      for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + c), __ldg(yr + c)));
-      v = acc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto load = [&](int buf, int k0) {
+    double* A = gsm + (buf * 2 + 0) * kGT * kGS;
+    double* B = gsm + (buf * 2 + 1) * kGT * kGS;
+    for (int e = tid; e < kGT * (kGK / 2); e += 128) {
+      const int r = e / (kGK / 2), c = (e % (kGK / 2)) * 2;
+      const int k = k0 + c;
+      const int ia = i0 + r, jb = j0 + r;
+      const bool oka = ia < rows && k < ld, okb = jb < cols && k < ld;
+      cp_async_16_zfill(A + r * kGS + c, ys + static_cast<size_t>(oka ? ia : 0) * ld + (oka ? k : 0), oka);
+      cp_async_16_zfill(B + r * kGS + c, xs + static_cast<size_t>(okb ? jb : 0) * ld + (okb ? k : 0), okb);
     }
-    t[e] = v;
+    cp_async_commit();
+  };
+
+  const int nk = (ld + kGK - 1) / kGK;
+  load(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nk) {
+      load(buf ^ 1, (kc + 1) * kGK);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* A = gsm + (buf * 2 + 0) * kGT * kGS + (wm * 32 + (lane >> 2)) * kGS + (lane & 3);
+    const double* B = gsm + (buf * 2 + 1) * kGT * kGS + (wn * 32 + (lane >> 2)) * kGS + (lane & 3);
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a[t] = A[t * 8 * kGS + k4];
+        b[t] = B[t * 8 * kGS + k4];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_884(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncthreads();
+  }
+  double* out = tab + pr * tab_stride;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int i = i0 + wm * 32 + mt * 8 + (lane >> 2);
+    if (i >= rows) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = j0 + wn * 32 + nt * 8 + 2 * (lane & 3);
+      if (j < cols) out[static_cast<size_t>(i) * cols + j] = acc[mt][nt][0];
+      if (j + 1 < cols) out[static_cast<size_t>(i) * cols + j + 1] = acc[mt][nt][1];
+    }
   }
 }
 
@@ -222,15 +299,23 @@ cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uin
 
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
-                             int bands, int dim, int ld, double* tab, unsigned long long tab_stride,
+                             int dim, int ld, bool exact, double* tab, unsigned long long tab_stride,
                              cudaStream_t st) {
   if (npairs == 0) return cudaSuccess;
-  const size_t per = static_cast<size_t>(bands) * (cols + 31) * 32;
-  const int threads = 256;
-  size_t bx = (per + threads - 1) / threads;
-  if (bx > 4096) bx = 4096;
-  const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(npairs));
-  rho_table_kernel<<<grid, threads, 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, bands, dim, ld, tab, tab_stride);
+  if (exact) {
+    const dim3 grid((cols + 31) / 32, (rows + 7) / 8, static_cast<unsigned>(npairs));
+    rho_table_exact_kernel<<<grid, dim3(32, 8), 0, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, dim, ld, tab,
+                                                         tab_stride);
+    return cudaGetLastError();
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(rho_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((cols + kGT - 1) / kGT, (rows + kGT - 1) / kGT, static_cast<unsigned>(npairs));
+  rho_gemm_kernel<<<grid, 128, kGemmSmem, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, ld, tab, tab_stride);
   return cudaGetLastError();
 }
 

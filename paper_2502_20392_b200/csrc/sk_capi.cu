@@ -169,6 +169,7 @@ struct DevBuf {
 struct StatRec {
   cudaEvent_t a, b;
   double tiles, flops;
+  bool table;  // rho-table GEMM (large d) rather than a sweep
 };
 
 struct Ctx {
@@ -181,8 +182,8 @@ struct Ctx {
       scan, wd;
   bool stats_on = false;
   std::vector<StatRec> stats;
-  uint64_t sweep_launches = 0, aux_launches = 0;
-  double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0;
+  uint64_t sweep_launches = 0, aux_launches = 0, table_launches = 0;
+  double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0, done_table_ms = 0.0;
 
   cudaStream_t stream() const { return user ? user : own; }
   ~Ctx() {
@@ -320,8 +321,8 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
   tr.mark("  occupancy+memgetinfo");
 
-  // large d: per-pair skewed rho tables, pairs chunked to a memory budget
-  const size_t tab_elems = dp == 0 ? static_cast<size_t>(bands) * (cols + 31) * 32 : 0;
+  // large d: per-pair rho tables (rows x cols), pairs chunked to a memory budget
+  const size_t tab_elems = dp == 0 ? static_cast<size_t>(rows) * cols : 0;
   size_t chunk = npairs_all;
   if (dp == 0) {
     const size_t budget = std::max<size_t>(free_b / 3, tab_elems * sizeof(double));
@@ -367,9 +368,16 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     if (bands > 1) SK_CUDA(c.abuf.ensure(slots * col_bytes));
     if (dp == 0) {
       SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
-      SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, bands, ps.dim,
-                               ps.ld, c.tab.as<double>(), tab_elems, c.stream()));
+      // exact (sequential) deltas when max|rho| is reported or the literal
+      // (bit-identical) kernel runs; DMMA tensor-core GEMM otherwise
+      StatRec trec{};
+      trec.table = true;
+      if (int rc = record_start(c, &trec, st)) return rc;
+      SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, ps.dim, ps.ld,
+                               exact || ntempl == 0, c.tab.as<double>(), tab_elems, c.stream()));
+      if (int rc = record_end(c, &trec, st)) return rc;
       ++c.aux_launches;
+      ++c.table_launches;
     }
     SweepParams P{};
     P.xinc = ps.d_xinc;
@@ -978,8 +986,8 @@ int sk_stats_reset(void) {
     cudaEventDestroy(r.b);
   }
   c->stats.clear();
-  c->sweep_launches = c->aux_launches = 0;
-  c->done_ms = c->done_tiles = c->done_flops = 0.0;
+  c->sweep_launches = c->aux_launches = c->table_launches = 0;
+  c->done_ms = c->done_tiles = c->done_flops = c->done_table_ms = 0.0;
   return SK_OK;
 }
 
@@ -991,9 +999,13 @@ int sk_stats_get(sk_stats* out) {
     cudaEventSynchronize(r.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
-    c->done_ms += ms;
-    c->done_tiles += r.tiles;
-    c->done_flops += r.flops;
+    if (r.table) {
+      c->done_table_ms += ms;
+    } else {
+      c->done_ms += ms;
+      c->done_tiles += r.tiles;
+      c->done_flops += r.flops;
+    }
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
@@ -1003,6 +1015,8 @@ int sk_stats_get(sk_stats* out) {
   out->sweep_ms = c->done_ms;
   out->tiles = c->done_tiles;
   out->tile_flops = c->done_flops;
+  out->table_launches = c->table_launches;
+  out->table_ms = c->done_table_ms;
   return SK_OK;
 }
 

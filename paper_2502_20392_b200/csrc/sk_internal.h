@@ -22,10 +22,11 @@ inline int pick_dp(size_t dim) {
 }
 
 // Device increment layout: per series `len` rows of `ld` doubles, row 0 zero,
-// row k+1 = dz_k zero-padded to ld (ld = pick_dp(d), or d on the table path).
+// row k+1 = dz_k zero-padded to ld (ld = pick_dp(d), or d rounded up to a
+// multiple of 4 on the table path: 16-byte rows, whole DMMA k-steps).
 inline size_t inc_ld(size_t dim) {
   const int dp = pick_dp(dim);
-  return dp > 0 ? static_cast<size_t>(dp) : dim;
+  return dp > 0 ? static_cast<size_t>(dp) : (dim + 3) / 4 * 4;
 }
 cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, size_t ld, double* out,
                               cudaStream_t st);
@@ -34,9 +35,11 @@ cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, s
 cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                                size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
                                int dim, int ld, unsigned long long* out, cudaStream_t st);
+// rho[i][j] tables (rows x cols, row-major) for the large-d path: DMMA GEMM,
+// or the bit-exact sequential dot when `exact`.
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
-                             int bands, int dim, int ld, double* tab, unsigned long long tab_stride,
+                             int dim, int ld, bool exact, double* tab, unsigned long long tab_stride,
                              cudaStream_t st);
 cudaError_t launch_grid_init(double* grid, size_t nout, size_t lx, size_t ly, cudaStream_t st);
 cudaError_t launch_step_tile_literal(double delta, int order, const double* w65, const double* in, double* out,

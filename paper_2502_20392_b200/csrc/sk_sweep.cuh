@@ -59,7 +59,7 @@ struct SweepParams {
   const uint32_t* pair_out;       // launch-local pair -> output slot
   unsigned long long sx, sy;      // elements between consecutive series
   const double* w65;              // N == 0: W table, row stride 65 (device memory)
-  const double* rho_tab;          // DP == 0: skewed delta table per launch-local pair
+  const double* rho_tab;          // DP == 0: rho table (rows x cols, row-major) per launch-local pair
   unsigned long long tab_stride;  // elements per pair in rho_tab
   int dim, order;                 // dim: logical d (row stride of the increments is DP)
   int rows, cols, bands, npairs, group, slots;
@@ -224,7 +224,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     yrow = P.yinc + P.pair_y[p] * P.sy + static_cast<size_t>(row_ok ? i + 1 : 0) * DP;
     xser = P.xinc + P.pair_x[p] * P.sx + DP;  // row j of the pair at xser + j * DP
   } else {
-    tab = P.rho_tab + static_cast<size_t>(p) * P.tab_stride + static_cast<size_t>(b) * (cols + 31) * 32;
+    tab = P.rho_tab + static_cast<size_t>(p) * P.tab_stride;  // rows x cols, row-major
   }
 
   // Loop-carried register state: this lane's beta (the left edge of its next
@@ -260,10 +260,17 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
         cp_async_16(s_ring + (col & (kRing - 1)) * XS + 2 * part, xser + static_cast<size_t>(col) * DP + 2 * part);
       }
     } else {
-      const int nst = max(0, min(kChunk, steps - col0));
-      const double* src = tab + static_cast<size_t>(col0) * 32;
-      double* dst = s_delta + (g & 1) * kChunk * 32;
-      for (int k = lane; k < nst * 16; k += 32) cp_async_16(dst + 2 * k, src + 2 * k);
+      // row-major rho table: lane t gathers rho(i, g K + k - t), k < K,
+      // zero-filled outside the pair (8-byte cp.async, consecutive lanes ->
+      // consecutive shared words)
+      double* dst = s_delta + (g & 1) * kChunk * 32 + lane;
+      const double* trow = tab + static_cast<size_t>(row_ok ? i : 0) * cols;
+#pragma unroll 4
+      for (int k = 0; k < kChunk; ++k) {
+        const int j = col0 + k - lane;
+        const bool ok = row_ok && j >= 0 && j < cols;
+        cp_async_8_zfill(dst + k * 32, trow + (ok ? j : 0), ok);
+      }
     }
     cp_async_commit();
   };

@@ -353,13 +353,28 @@ def propagate_grid(x, y, order: int, options: Optional[PropagateOptions] = None)
 def propagate_with_policy(x, y, policy: TruncationPolicy, options: Optional[PropagateOptions] = None) -> KernelResult:
     """wavefront.hpp:51-53 (wavefront.cpp:206-221)."""
     x, y = _as_series(x), _as_series(y)
-    order, converged = policy.order, True
-    if policy.mode == "adaptive":
-        est = estimate_order(IncrementTable(x, y).max_abs_rho(), max(x.length(), y.length()), policy.tol)
-        order, converged = est.order, est.converged
-    r = propagate(x, y, order, options)
-    r.order_converged = converged
-    return r
+    if policy.mode != "adaptive":
+        return propagate(x, y, policy.order, options)
+    if x.dim() != y.dim():
+        raise ValueError("propagate: series dimensions differ")
+    # one batched call: the device order pre-pass proves N from a Cauchy-Schwarz
+    # bound of max|rho| and only runs the exact O(l^2 d) scan when it must
+    lib = _capi.load()
+    st = _capi.SkStatus()
+    per = _capi.SkStatus()
+    value = np.zeros(1)
+    order = np.zeros(1, dtype=np.int32)
+    conv = np.zeros(1, dtype=np.int32)
+    xv, yv = x.values(), y.values()
+    rc = lib.sk_pairwise(_ptr(xv), x.length(), _ptr(yv), y.length(), 1, x.dim(), 1, 7, float(policy.tol),
+                         _flags(options), _ptr(value), _ptr(order), _ptr(conv), None, ctypes.byref(per),
+                         ctypes.byref(st))
+    _check(rc, st)
+    if per.code != 0:
+        _raise(per)
+    lx, ly = x.length(), y.length()
+    return KernelResult(value=float(value[0]), order=int(order[0]), order_converged=bool(conv[0]),
+                        tiles_processed=(lx - 1) * (ly - 1), peak_live_series=_peak_live(ly - 1, lx - 1))
 
 
 def step_tile(delta: float, alpha, beta, order: int, fast: bool = False):
@@ -554,4 +569,5 @@ def stats_get() -> dict:
     s = _capi.SkStats()
     _capi.load().sk_stats_get(ctypes.byref(s))
     return {"sweep_launches": s.sweep_launches, "aux_launches": s.aux_launches, "sweep_ms": s.sweep_ms,
-            "tiles": s.tiles, "tile_flops": s.tile_flops}
+            "tiles": s.tiles, "tile_flops": s.tile_flops, "table_launches": s.table_launches,
+            "table_ms": s.table_ms}
