@@ -310,7 +310,8 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   const int na = ntempl > 0 ? ntempl + 1 : kMaxOrder + 1;
   const int np = (na + 1) & ~1;
   const int rows = ps.rows, cols = ps.cols;
-  const int bands = (rows + 31) / 32;
+  const int band_rows = 32 * rows_per_lane(ntempl);  // 64-row bands for the register kernels
+  const int bands = (rows + band_rows - 1) / band_rows;
   int bps = 0;
   const bool exact = o.d_maxrho != nullptr;
   const bool extras = o.d_grid != nullptr || o.d_diag != nullptr;

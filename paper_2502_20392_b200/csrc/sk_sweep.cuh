@@ -38,9 +38,7 @@
 
 namespace skb {
 
-constexpr int kChunk = 16;        // columns per staging group
 constexpr int kPublish = 32;      // columns per progress publication
-constexpr int kRing = 64;         // dx ring rows (>= 2 kChunk + 32)
 #ifndef SK_SWEEP_WARPS
 #define SK_SWEEP_WARPS 1
 #endif
@@ -50,6 +48,21 @@ constexpr int kSweepWarps = SK_SWEEP_WARPS;
 #ifndef SK_MIN_BLOCKS
 #define SK_MIN_BLOCKS 1
 #endif
+
+// Rows per lane.  R = 2: a warp sweeps a 64-row band, lane t owning rows t
+// and t + 32 (the second tile 32 columns behind the first), so two
+// independent tiles per step share the per-step overhead.  Measured on B200
+// (N = 8, d = 8, 256 x 4096^2): R = 1 68 ms, R = 2 77 ms (200 registers, 8
+// warps/SM, smaller chunks) -- R = 1 is the default; the literal kernel
+// (N = 0, series in local memory) always uses R = 1.
+#ifndef SK_ROWS_PER_LANE
+#define SK_ROWS_PER_LANE 1
+#endif
+__host__ __device__ constexpr int rows_per_lane(int N) { return N > 0 ? SK_ROWS_PER_LANE : 1; }
+// columns per staging group / delta batch
+__host__ __device__ constexpr int chunk_cols(int R) { return R == 2 ? 8 : 16; }
+// dx ring rows (power of two >= 32 R + 2 chunk)
+__host__ __device__ constexpr int ring_rows(int R) { return R == 2 ? 128 : 64; }
 
 struct SweepParams {
   const double* xinc;             // increments of the column series (first series, x)
@@ -85,12 +98,14 @@ __host__ __device__ constexpr int col_stride(int N) { return (series_len(N) + 1)
 // dx ring row stride in doubles: 16-byte rows padded so that the 8 lanes of
 // an LDS.128 phase (columns j, j-1, ..., j-7) hit distinct bank groups.
 __host__ __device__ constexpr int ring_stride(int DP) { return DP <= 2 ? 2 : DP + 2; }
-// per warp: band-below alpha stage (2 groups) | lane-to-lane alpha slots (2 x 32)
-// | lane 31's outputs of the chunk | dx ring (DP > 0) | delta stage (1 group
-// computed in place for DP > 0, 2 groups copied from the table for DP = 0)
+// per warp: band-below alpha stage (2 groups) | lane-to-lane alpha slots
+// (32 R) | lane 31's top-row outputs of the chunk | dx ring (DP > 0) | delta
+// stage (R x chunk x 32; x2 for the asynchronously staged table, DP = 0)
 __host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP) {
-  return 2 * kChunk * col_stride(N) + 2 * 32 * col_stride(N) + kChunk * col_stride(N) +
-         (DP > 0 ? kRing * ring_stride(DP) + kChunk * 32 : 2 * kChunk * 32);
+  return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + 32 * rows_per_lane(N) * col_stride(N) +
+         chunk_cols(rows_per_lane(N)) * col_stride(N) +
+         (DP > 0 ? ring_rows(rows_per_lane(N)) * ring_stride(DP) : 0) +
+         (DP > 0 ? 1 : 2) * rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32;
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -181,22 +196,22 @@ __device__ __forceinline__ void sts_series(double* dst, const double (&v)[NA], i
 template <int N, int DP, bool EXACT, bool EXTRAS>
 __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, unsigned b, int lane,
                                            double* __restrict__ smem) {
+  constexpr int R = rows_per_lane(N);
+  constexpr int K = chunk_cols(R);
+  constexpr int RING = ring_rows(R);
   constexpr int NA = series_len(N);
   constexpr int NP = col_stride(N);
   constexpr int XS = ring_stride(DP);
-  constexpr int kStage = kChunk * NP;
-  double* s_alpha = smem;                                   // 2 x kChunk x NP
-  double* s_pass = s_alpha + 2 * kStage;                    // 2 x 32 x NP (step parity)
-  double* s_out = s_pass + 64 * NP;                         // kChunk x NP
-  double* s_ring = s_out + kStage;                          // kRing x XS (DP > 0)
-  double* s_delta = s_ring + (DP > 0 ? kRing * XS : 0);     // kChunk x 32 (x2 for DP = 0)
+  constexpr int kStage = K * NP;
+  double* s_alpha = smem;                                   // 2 x K x NP
+  double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
+  double* s_out = s_pass + 32 * R * NP;                     // K x NP
+  double* s_ring = s_out + kStage;                          // RING x XS (DP > 0)
+  double* s_delta = s_ring + (DP > 0 ? RING * XS : 0);      // [buf][r][k][lane]
   const int n = N > 0 ? N + 1 : P.order + 1;
   const int rows = P.rows, cols = P.cols;
-  const int row0 = static_cast<int>(b) * 32;
-  const int rb = min(32, rows - row0);
-  const int i = row0 + lane;
-  const bool row_ok = lane < rb;
-  const bool last_row = row_ok && i == rows - 1;
+  const int row0 = static_cast<int>(b) * 32 * R;
+  const int rb = min(32 * R, rows - row0);
   const unsigned slot = p % static_cast<unsigned>(P.slots);
   const unsigned long long base = static_cast<unsigned long long>(p) * static_cast<unsigned long long>(cols + 1);
   double* colbuf = P.abuf + static_cast<size_t>(slot) * static_cast<size_t>(cols) * NP;
@@ -216,35 +231,43 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
       return;
   }
 
-  // increments are stored with row stride DP behind one leading zero row
-  const double* yrow = nullptr;
-  const double* xser = nullptr;
-  const double* tab = nullptr;
-  if constexpr (DP > 0) {
-    yrow = P.yinc + P.pair_y[p] * P.sy + static_cast<size_t>(row_ok ? i + 1 : 0) * DP;
-    xser = P.xinc + P.pair_x[p] * P.sx + DP;  // row j of the pair at xser + j * DP
-  } else {
-    tab = P.rho_tab + static_cast<size_t>(p) * P.tab_stride;  // rows x cols, row-major
-  }
-
-  // Loop-carried register state: this lane's beta (the left edge of its next
-  // tile).  Before a lane's first column (j < 0) it runs the delta = 0 tile
-  // on unit series, whose output is the unit series again, so beta is e0
-  // exactly at j = 0 without a select (the alpha slots start at e0 too).
-  double roA[NA], roB[NA];
+  // per tile r of this lane: row i_r = row0 + 32 r + lane, column s - lane - 32 r
+  int irow[R];
+  bool row_ok[R], last_row[R];
+  const double* yrow[R];
 #pragma unroll
-  for (int m = 0; m < NA; ++m) roA[m] = (m == 0) ? 1.0 : 0.0;
+  for (int r = 0; r < R; ++r) {
+    irow[r] = row0 + 32 * r + lane;
+    row_ok[r] = 32 * r + lane < rb;
+    last_row[r] = row_ok[r] && irow[r] == rows - 1;
+    // increments are stored with row stride DP behind one leading zero row
+    yrow[r] = DP > 0 ? P.yinc + P.pair_y[p] * P.sy + static_cast<size_t>(row_ok[r] ? irow[r] + 1 : 0) * DP : nullptr;
+  }
+  const double* xser = DP > 0 ? P.xinc + P.pair_x[p] * P.sx + DP : nullptr;  // row j at xser + j * DP
+  const double* tab = DP > 0 ? nullptr : P.rho_tab + static_cast<size_t>(p) * P.tab_stride;  // rows x cols
+
+  // Loop-carried register state: each tile's beta (the left edge of its next
+  // tile), ping-ponged between A and B.  Before a tile's first column it runs
+  // the delta = 0 tile on unit series, whose output is the unit series again,
+  // so beta is e0 exactly at its first column without a select.
+  double roA[R][NA], roB[R][NA];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int m = 0; m < NA; ++m) roA[r][m] = (m == 0) ? 1.0 : 0.0;
   double mx = 0.0;
-  unsigned jkey = ~0u;  // (first failing column << 2) | code for this lane
+  unsigned jkey[R];  // (first failing column << 2) | code, per tile
+#pragma unroll
+  for (int r = 0; r < R; ++r) jkey[r] = ~0u;
   unsigned long long seen = 0;
   const int steps = cols + rb - 1;
 
   // ---- staging: group g = steps/columns [g K, g K + K): band-below alpha
-  // (2 buffers), dx (ring row = column mod kRing) or, on the table path, the
+  // (2 buffers), dx (ring row = column mod RING) or, on the table path, the
   // deltas of those steps (2 buffers); one cp.async group per g.
   auto stage_group = [&](int g) {
-    const int col0 = g * kChunk;
-    const int ncol = max(0, min(kChunk, cols - col0));
+    const int col0 = g * K;
+    const int ncol = max(0, min(K, cols - col0));
     if (has_below) {
       const double* src = colbuf + static_cast<size_t>(col0) * NP;
       double* dst = s_alpha + (g & 1) * kStage;
@@ -257,19 +280,22 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
       for (int k = lane; k < pieces; k += 32) {
         const int c = k / PR, part = k - c * PR;
         const int col = col0 + c;
-        cp_async_16(s_ring + (col & (kRing - 1)) * XS + 2 * part, xser + static_cast<size_t>(col) * DP + 2 * part);
+        cp_async_16(s_ring + (col & (RING - 1)) * XS + 2 * part, xser + static_cast<size_t>(col) * DP + 2 * part);
       }
     } else {
-      // row-major rho table: lane t gathers rho(i, g K + k - t), k < K,
+      // row-major rho table: tile r of lane t gathers rho(i_r, g K + k - t - 32 r),
       // zero-filled outside the pair (8-byte cp.async, consecutive lanes ->
       // consecutive shared words)
-      double* dst = s_delta + (g & 1) * kChunk * 32 + lane;
-      const double* trow = tab + static_cast<size_t>(row_ok ? i : 0) * cols;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double* dst = s_delta + ((g & 1) * R + r) * K * 32 + lane;
+        const double* trow = tab + static_cast<size_t>(row_ok[r] ? irow[r] : 0) * cols;
 #pragma unroll 4
-      for (int k = 0; k < kChunk; ++k) {
-        const int j = col0 + k - lane;
-        const bool ok = row_ok && j >= 0 && j < cols;
-        cp_async_8_zfill(dst + k * 32, trow + (ok ? j : 0), ok);
+        for (int k = 0; k < K; ++k) {
+          const int j = col0 + k - lane - 32 * r;
+          const bool ok = row_ok[r] && j >= 0 && j < cols;
+          cp_async_8_zfill(dst + k * 32, trow + (ok ? j : 0), ok);
+        }
       }
     }
     cp_async_commit();
@@ -278,66 +304,70 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     // band 0: the bottom edge of the domain is the unit series in every column
     for (int e = lane; e < 2 * kStage; e += 32) s_alpha[e] = (e % NP == 0) ? 1.0 : 0.0;
   }
-  for (int e = lane; e < 64 * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
+  for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
   if constexpr (DP > 0) {
-    // columns -32..-1 (ring rows 32..63): zero increments => delta = 0
-    for (int e = lane; e < 32 * XS; e += 32) s_ring[32 * XS + e] = 0.0;
+    // columns -RING/2..-1 (ring rows RING/2..RING-1): zero increments => delta = 0
+    for (int e = lane; e < (RING / 2) * XS; e += 32) s_ring[(RING / 2) * XS + e] = 0.0;
   }
   __syncwarp();
-  if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, kChunk), seen, p, b)) return;
+  if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, K), seen, p, b)) return;
   stage_group(0);
 
-  // step s writes slot [s & 1][lane] and reads [(s - 1) & 1][lane - 1]: the
-  // double buffer needs only one __syncwarp per step (RAW); the WAR reuse
-  // two steps later is ordered by the intervening one
-  double* const my_pass = s_pass + lane * NP;
-  const double* const below_pass = s_pass + (lane - 1) * NP;
-
-  // one tile step: column j = s - lane of row i
-  auto step = [&](int s, int k, int par, const double* stage, double delta, double (&r_in)[NA],
-                  double (&ro_out)[NA]) {
-    const int j = s - lane;
-    double q[NA], qo[NA];
-    // alpha: lane 0 from the band below (stage), lane t from lane t-1's slot
-    lds_series<NA>(lane == 0 ? stage + k * NP : below_pass + (par ^ 1) * 32 * NP, q, n);
-
-    double total;
-    if constexpr (N > 0) {
-      total = tile_step_scaled<N>(q, r_in, delta, qo, ro_out, fault);
-    } else {
-      total = tile_step_literal(P.order, q, r_in, delta, P.w65, qo, ro_out);
+  // one step = R tiles of this lane (one basic block, conditional work predicated)
+  auto step = [&](int s, int k, const double* stage, const double* dl, double (&r_in)[R][NA],
+                  double (&ro_out)[R][NA]) {
+    double q[R][NA];
+    // alpha: lane 0's first tile from the band below (stage); every other
+    // tile from the slot of the row below -- slot index (32 r + t) - 1, so
+    // lane 0's tile r >= 1 reads lane 31's tile r - 1
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double* src = (r == 0 && lane == 0) ? stage + k * NP : s_pass + (32 * r + lane - 1) * NP;
+      lds_series<NA>(src, q[r], n);
     }
-    // alpha' up: lane 31 parks it for the band above, the others in their slot
-    sts_series<NA>(lane == 31 ? s_out + k * NP : my_pass + par * 32 * NP, qo, n);
-    __syncwarp();
+    __syncwarp();  // every slot has been read before any is rewritten
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int j = s - lane - 32 * r;
+      const double delta = dl[(r * K + k) * 32 + lane];
+      double qo[NA];
+      double total;
+      if constexpr (N > 0) {
+        total = tile_step_scaled<N>(q[r], r_in[r], delta, qo, ro_out[r], fault);
+      } else {
+        total = tile_step_literal(P.order, q[r], r_in[r], delta, P.w65, qo, ro_out[r]);
+      }
+      // alpha' up: the band's top row (lane 31, last tile) parks it for the
+      // band above, every other row in its slot
+      sts_series<NA>((r == R - 1 && lane == 31) ? s_out + k * NP : s_pass + (32 * r + lane) * NP, qo, n);
 
-#ifndef SK_EXPERIMENT_NO_CHECKS
-    const bool active = row_ok && j >= 0 && j < cols;
-    // the reference's throw order inside a tile: delta guard (checked when
-    // the chunk's deltas are formed), corner check, non-finite total
-    // (wavefront.cpp:150-173); the first failing tile of the lane wins
-    const unsigned code = (strict && corner_mismatch(q[0], r_in[0])) ? kErrCorner
-                          : !isfinite(total)                         ? kErrNonFinite
-                                                                     : 0u;
-    const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
-    jkey = (active && code != 0u && kk < jkey) ? kk : jkey;
-#else
-    const bool active = row_ok && j >= 0 && j < cols;
-#endif
-    st_global_if(last_row && j == cols - 1, P.values + out, total);
-    if constexpr (EXTRAS) {
-      if (P.grid)
-        st_global_if(active, P.grid + out * P.grid_stride + static_cast<size_t>(j + 1) * (rows + 1) + (i + 1), total);
-      if (P.diag) st_global_if(active && i == j, P.diag + out * P.diag_stride + i, total);
+      const bool active = row_ok[r] && j >= 0 && j < cols;
+      // the reference's throw order inside a tile: delta guard (checked when
+      // the chunk's deltas are formed), corner check, non-finite total
+      // (wavefront.cpp:150-173); the first failing tile of the row wins
+      const unsigned code = (strict && corner_mismatch(q[r][0], r_in[r][0])) ? kErrCorner
+                            : !isfinite(total)                               ? kErrNonFinite
+                                                                             : 0u;
+      const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
+      jkey[r] = (active && code != 0u && kk < jkey[r]) ? kk : jkey[r];
+      st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
+      if constexpr (EXTRAS) {
+        if (P.grid)
+          st_global_if(active,
+                       P.grid + out * P.grid_stride + static_cast<size_t>(j + 1) * (rows + 1) + (irow[r] + 1),
+                       total);
+        if (P.diag) st_global_if(active && irow[r] == j, P.diag + out * P.diag_stride + irow[r], total);
+      }
     }
+    __syncwarp();  // slots written before the next step reads them
   };
 
-  const int ngroups_in = (cols + kChunk - 1) / kChunk;
-  const int ngroups = DP > 0 ? ngroups_in : (steps + kChunk - 1) / kChunk;
-  for (int c0 = 0, chunk = 0; c0 < steps; c0 += kChunk, ++chunk) {
+  const int ngroups_in = (cols + K - 1) / K;
+  const int ngroups = DP > 0 ? ngroups_in : (steps + K - 1) / K;
+  for (int c0 = 0, chunk = 0; c0 < steps; c0 += K, ++chunk) {
     __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
     if (chunk + 1 < ngroups) {
-      if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, (chunk + 2) * kChunk), seen, p, b))
+      if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, (chunk + 2) * K), seen, p, b))
         return;
       stage_group(chunk + 1);
       cp_async_wait<1>();
@@ -346,30 +376,30 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     }
     __syncwarp();
     const double* stage = s_alpha + (chunk & 1) * kStage;
-    const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * kChunk * 32);
-    const int kend = min(kChunk, steps - c0);
-    // the chunk's increment products (lane t, step c0 + k -> column c0 + k - t)
-    // with the delta guard (wavefront.cpp:150-155) and max|delta|
-    {
+    const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * R * K * 32);
+    const int kend = min(K, steps - c0);
+    // the chunk's increment products (tile r, step c0 + k -> column
+    // c0 + k - t - 32 r) with the delta guard (wavefront.cpp:150-155) and max|delta|
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
       double dy[DP > 0 ? DP : 1];
       if constexpr (DP > 0) {
 #pragma unroll
         for (int c = 0; c < DP; c += 2) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(yrow + c));
+          const double2 v = __ldg(reinterpret_cast<const double2*>(yrow[r] + c));
           dy[c] = v.x;
           dy[c + 1] = v.y;
         }
       }
 #pragma unroll 1
-      for (int k0 = 0; k0 < kChunk; k0 += 4) {
+      for (int k0 = 0; k0 < K; k0 += 4) {
         double dd[4];
         if constexpr (DP > 0) {
-          // four columns at a time: all loads first, then four independent
-          // two-accumulator dots
+          // four columns at a time: all loads first, then four independent dots
           double dx[4][DP];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const double* xr = s_ring + ((c0 + k0 + u - lane) & (kRing - 1)) * XS;
+            const double* xr = s_ring + ((c0 + k0 + u - lane - 32 * r) & (RING - 1)) * XS;
 #pragma unroll
             for (int c = 0; c < DP; c += 2) {
               const double2 v = *reinterpret_cast<const double2*>(xr + c);
@@ -390,21 +420,21 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
               }
               dd[u] = e0 + e1;
             }
-            s_delta[(k0 + u) * 32 + lane] = dd[u];
+            s_delta[(r * K + k0 + u) * 32 + lane] = dd[u];
           }
         } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dd[u] = dl[(k0 + u) * 32 + lane];
+          for (int u = 0; u < 4; ++u) dd[u] = dl[(r * K + k0 + u) * 32 + lane];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int k = k0 + u;
-          const int j = c0 + k - lane;
-          const bool act = row_ok && j >= 0 && j < cols && k < kend;
+          const int j = c0 + k - lane - 32 * r;
+          const bool act = row_ok[r] && j >= 0 && j < cols && k < kend;
           const double ad = fabs(dd[u]);
           if constexpr (EXACT) mx = fmax(mx, act ? ad : 0.0);
           const unsigned kk = (static_cast<unsigned>(j) << 2) | kErrDelta;
-          jkey = (act && !(ad <= kDeltaOverflowLimit) && kk < jkey) ? kk : jkey;
+          jkey[r] = (act && !(ad <= kDeltaOverflowLimit) && kk < jkey[r]) ? kk : jkey[r];
         }
       }
     }
@@ -412,20 +442,20 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     int k = 0;
 #pragma unroll 1
     for (; k + 1 < kend; k += 2) {
-      const double d0 = dl[k * 32 + lane];
-      const double d1 = dl[(k + 1) * 32 + lane];
-      step(c0 + k, k, 0, stage, d0, roA, roB);
-      step(c0 + k + 1, k + 1, 1, stage, d1, roB, roA);
+      step(c0 + k, k, stage, dl, roA, roB);
+      step(c0 + k + 1, k + 1, stage, dl, roB, roA);
     }
     if (k < kend) {
-      step(c0 + k, k, k & 1, stage, dl[k * 32 + lane], roA, roB);
+      step(c0 + k, k, stage, dl, roA, roB);
 #pragma unroll
-      for (int m = 0; m < NA; ++m) roA[m] = roB[m];
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < NA; ++m) roA[r][m] = roB[r][m];
     }
-    // hand lane 31's alpha' of this chunk (columns c0 - 31 .. c0 + kend - 32)
-    // to the band above, then publish progress every kPublish columns
+    // hand the top row's alpha' of this chunk to the band above, then publish
+    // progress every kPublish columns
     if (has_above) {
-      const int jfirst = c0 - 31;
+      const int jfirst = c0 - 31 - 32 * (R - 1);
       const int pieces = kend * NP / 2;
       for (int e = lane; e < pieces; e += 32) {
         const int kk = e / (NP / 2);
@@ -436,8 +466,8 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
         }
       }
       // columns handed up before / after this chunk
-      const int done0 = min(max(c0 - 31, 0), cols);
-      const int done1 = min(max(c0 + kend - 31, 0), cols);
+      const int done0 = min(max(jfirst, 0), cols);
+      const int done1 = min(max(jfirst + kend, 0), cols);
       if (done1 > done0 && (done1 == cols || done1 / kPublish != done0 / kPublish)) {
         __threadfence();
         __syncwarp();
@@ -452,7 +482,9 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     __syncwarp();
     if (lane == 0) st_release_gpu(prog_row + b, base + cols);
   }
-  if (jkey != ~0u) atomicMin(P.err + out, err_key(i, jkey >> 2, jkey & 3u));
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (jkey[r] != ~0u) atomicMin(P.err + out, err_key(irow[r], jkey[r] >> 2, jkey[r] & 3u));
   if constexpr (EXACT) {
     if (P.maxrho) {
 #pragma unroll
