@@ -132,6 +132,30 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
  * because the family is padded to one length).  Host arithmetic only. */
 int sk_gram_shard_range(size_t m, size_t shard, size_t nshards, size_t* first, size_t* last);
 
+/* ---- Multi-GPU long pair: strip pipeline (cfg 3).
+ * The ly-1 tile rows are cut into bands of 32*R rows (sk_strip_bands); GPU g
+ * sweeps a contiguous band range and hands its top band's alpha series to
+ * GPU g+1 through an exchange buffer in GPU g+1's memory (peer stores over
+ * NVLink, system-scope release / acquire on a progress counter).  Setup: the
+ * consumer allocates (sk_exchange_alloc) and exports (sk_ipc_handle) its
+ * buffer; the producer maps it (sk_ipc_open).  All strips run concurrently. */
+int sk_strip_bands(size_t ly, int order, size_t* bands);
+int sk_exchange_alloc(size_t lx, int order, void** abuf, void** prog, sk_status* st);
+int sk_exchange_reset(void* prog, sk_status* st);
+int sk_exchange_free(void* abuf, void* prog);
+int sk_ipc_handle(void* dptr, void* handle64, sk_status* st);
+int sk_ipc_open(const void* handle64, void** dptr, sk_status* st);
+int sk_ipc_close(void* dptr);
+int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
+                       uint32_t flags, size_t band_begin, size_t band_end, const void* in_abuf,
+                       const void* in_prog, void* out_abuf, void* out_prog, double* value, double* diag,
+                       sk_status* st);
+/* One-GPU emulation of a two-strip pipeline (single launch; the hand-off from
+ * band split_band-1 to split_band goes through an exchange buffer with the
+ * multi-GPU protocol).  Test entry point. */
+int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
+                       uint32_t flags, size_t split_band, double* value, sk_status* st);
+
 /* Device-time accounting of the sweep kernels on the calling thread
  * (CUDA events around every sweep launch). */
 typedef struct sk_stats {

@@ -29,6 +29,8 @@ EXPORTED = [
     "sk_propagate", "sk_max_abs_rho", "sk_estimate_order", "sk_step_tile",
     "sk_step_tile_fast", "sk_pairwise", "sk_pairwise_device", "sk_gram", "sk_gram_shard_range",
     "sk_stats_enable", "sk_stats_reset", "sk_stats_get", "sk_release",
+    "sk_strip_bands", "sk_exchange_alloc", "sk_exchange_reset", "sk_exchange_free", "sk_ipc_handle",
+    "sk_ipc_open", "sk_ipc_close", "sk_propagate_strip", "sk_propagate_split",
 ]
 
 
@@ -84,6 +86,16 @@ def load():
         "sk_stats_reset": ([], ctypes.c_int),
         "sk_stats_get": ([ctypes.POINTER(SkStats)], ctypes.c_int),
         "sk_release": ([], ctypes.c_int),
+        "sk_strip_bands": ([SZ, ctypes.c_int, P], ctypes.c_int),
+        "sk_exchange_alloc": ([SZ, ctypes.c_int, P, P, ST], ctypes.c_int),
+        "sk_exchange_reset": ([P, ST], ctypes.c_int),
+        "sk_exchange_free": ([P, P], ctypes.c_int),
+        "sk_ipc_handle": ([P, P, ST], ctypes.c_int),
+        "sk_ipc_open": ([P, P, ST], ctypes.c_int),
+        "sk_ipc_close": ([P], ctypes.c_int),
+        "sk_propagate_strip": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, SZ, P, P, P, P, P, P, ST],
+                               ctypes.c_int),
+        "sk_propagate_split": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, P, ST], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

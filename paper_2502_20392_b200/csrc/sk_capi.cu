@@ -299,10 +299,22 @@ int check_watchdog(Ctx& c, sk_status* st) {
                     h[3], h[4]);
 }
 
+// A band range of one pair plus its cross-strip hand-off (multi-GPU long
+// pair, SweepParams::xin_* / xout_*).  Default: every band, no hand-off.
+struct Strip {
+  int band_begin = 0, band_end = -1;
+  int xin_band = -1, xout_band = -1;
+  const double* xin_abuf = nullptr;
+  const unsigned long long* xin_prog = nullptr;
+  double* xout_abuf = nullptr;
+  unsigned long long* xout_prog = nullptr;
+};
+
 // One persistent sweep launch per (order, pair chunk).  px/py/pout are
 // launch-local pair lists of equal length.
 int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const std::vector<uint32_t>& py,
-               const std::vector<uint32_t>& pout, int order, uint32_t flags, const Outputs& o, sk_status* st) {
+               const std::vector<uint32_t>& pout, int order, uint32_t flags, const Outputs& o, sk_status* st,
+               const Strip& strip = Strip{}) {
   const size_t npairs_all = px.size();
   if (npairs_all == 0) return SK_OK;
   const int ntempl = order <= kMaxRegOrder ? order : 0;
@@ -334,7 +346,8 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
 
   for (size_t c0 = 0; c0 < npairs_all; c0 += chunk) {
     const size_t npairs = std::min(chunk, npairs_all - c0);
-    const unsigned long long units = static_cast<unsigned long long>(npairs) * bands;
+    const int nb = (strip.band_end < 0 ? bands : strip.band_end) - strip.band_begin;
+    const unsigned long long units = static_cast<unsigned long long>(npairs) * nb;
     int blocks = bps * c.sms;
     const unsigned long long need_blocks = (units + kSweepWarps - 1) / kSweepWarps;
     if (static_cast<unsigned long long>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
@@ -412,6 +425,14 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.diag = o.d_diag;
     P.grid_stride = o.grid_stride;
     P.diag_stride = o.diag_stride;
+    P.band_begin = strip.band_begin;
+    P.band_end = strip.band_end < 0 ? bands : strip.band_end;
+    P.xin_band = strip.xin_band;
+    P.xout_band = strip.xout_band;
+    P.xin_abuf = strip.xin_abuf;
+    P.xin_prog = strip.xin_prog;
+    P.xout_abuf = strip.xout_abuf;
+    P.xout_prog = strip.xout_prog;
 
     StatRec rec{};
     rec.tiles = static_cast<double>(npairs) * rows * cols;
@@ -959,6 +980,199 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
   if (max_product) *max_product = best;
   if (first_fatal >= 0) return decode_err(he[first_fatal], st, nullptr, nullptr, dim);
   return SK_OK;
+}
+
+// ------------------------------------------------------ multi-GPU strips
+static int np_of(int order) { return col_stride(order <= kMaxRegOrder ? order : 0); }
+
+int sk_strip_bands(size_t ly, int order, size_t* bands) {
+  if (ly < 2 || order < 1 || order > kMaxOrder) return SK_INVALID_ARGUMENT;
+  const size_t band_rows = 32 * static_cast<size_t>(rows_per_lane(order <= kMaxRegOrder ? order : 0));
+  *bands = (ly - 1 + band_rows - 1) / band_rows;
+  return SK_OK;
+}
+
+int sk_exchange_alloc(size_t lx, int order, void** abuf, void** prog, sk_status* st) {
+  clear_status(st);
+  if (lx < 2 || order < 1 || order > kMaxOrder)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "exchange: bad length/order");
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  const size_t bytes = (lx - 1) * np_of(order) * sizeof(double);
+  SK_CUDA(cudaMalloc(abuf, bytes));
+  SK_CUDA(cudaMalloc(prog, 256));
+  SK_CUDA(cudaMemset(*prog, 0, 256));
+  return SK_OK;
+}
+
+int sk_exchange_reset(void* prog, sk_status* st) {
+  clear_status(st);
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  SK_CUDA(cudaMemset(prog, 0, 256));
+  return SK_OK;
+}
+
+int sk_exchange_free(void* abuf, void* prog) {
+  if (abuf) cudaFree(abuf);
+  if (prog) cudaFree(prog);
+  return SK_OK;
+}
+
+int sk_ipc_handle(void* dptr, void* handle64, sk_status* st) {
+  clear_status(st);
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  cudaIpcMemHandle_t h;
+  SK_CUDA(cudaIpcGetMemHandle(&h, dptr));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, sizeof h);
+  return SK_OK;
+}
+
+int sk_ipc_open(const void* handle64, void** dptr, sk_status* st) {
+  clear_status(st);
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  SK_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SK_OK;
+}
+
+int sk_ipc_close(void* dptr) {
+  cudaIpcCloseMemHandle(dptr);
+  return SK_OK;
+}
+
+// One strip of a long pair: bands [band_begin, band_end) of the 32R-row bands
+// (sk_strip_bands).  The bottom band (band_begin > 0) reads its alpha from
+// in_abuf / in_prog (device memory of this GPU, written by the previous
+// strip's GPU); the top band (band_end < bands) writes to out_abuf / out_prog
+// (the next GPU's exchange buffer, a peer pointer from sk_ipc_open).  All
+// strips of a pair run concurrently, one per GPU.  *value is written only by
+// the strip that owns the last row; diag (optional, min(lx,ly)-1 entries)
+// receives this strip's knots.
+int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
+                       size_t band_begin, size_t band_end, const void* in_abuf, const void* in_prog, void* out_abuf,
+                       void* out_prog, double* value, double* diag, sk_status* st) {
+  clear_status(st);
+  size_t bands = 0;
+  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: bad arguments");
+  if (band_begin >= band_end || band_end > bands)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: band range [%zu, %zu) outside [0, %zu)",
+                      band_begin, band_end, bands);
+  if ((band_begin > 0) != (in_abuf != nullptr) || (band_end < bands) != (out_abuf != nullptr))
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: exchange buffers do not match the range");
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  const size_t ld = inc_ld(dim);
+  SK_CUDA(c.raw_x.ensure(lx * dim * sizeof(double)));
+  SK_CUDA(c.raw_y.ensure(ly * dim * sizeof(double)));
+  SK_CUDA(c.xinc.ensure(lx * ld * sizeof(double)));
+  SK_CUDA(c.yinc.ensure(ly * ld * sizeof(double)));
+  SK_CUDA(c.values.ensure(sizeof(double)));
+  SK_CUDA(cudaMemcpyAsync(c.raw_x.p, x, lx * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(c.raw_y.p, y, ly * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(launch_increments(c.raw_x.as<double>(), 1, lx, dim, ld, c.xinc.as<double>(), c.stream()));
+  SK_CUDA(launch_increments(c.raw_y.as<double>(), 1, ly, dim, ld, c.yinc.as<double>(), c.stream()));
+  c.aux_launches += 2;
+  SK_CUDA(c.err.ensure(sizeof(unsigned long long)));
+  SK_CUDA(cudaMemsetAsync(c.err.p, 0xff, sizeof(unsigned long long), c.stream()));
+  SK_CUDA(cudaMemsetAsync(c.values.p, 0xff, sizeof(double), c.stream()));
+  const size_t nd = std::min(lx, ly) - 1;
+  double* d_diag = nullptr;
+  if (diag) {
+    SK_CUDA(c.diag.ensure(nd * sizeof(double)));
+    d_diag = c.diag.as<double>();
+    SK_CUDA(cudaMemsetAsync(d_diag, 0xff, nd * sizeof(double), c.stream()));
+  }
+  PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), lx * ld, ly * ld, static_cast<int>(ly - 1),
+             static_cast<int>(lx - 1), static_cast<int>(dim), static_cast<int>(ld)};
+  Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(), nullptr, nullptr, d_diag, lx * ly, nd};
+  Strip s;
+  s.band_begin = static_cast<int>(band_begin);
+  s.band_end = static_cast<int>(band_end);
+  if (band_begin > 0) {
+    s.xin_band = static_cast<int>(band_begin);
+    s.xin_abuf = static_cast<const double*>(in_abuf);
+    s.xin_prog = static_cast<const unsigned long long*>(in_prog);
+  }
+  if (band_end < bands) {
+    s.xout_band = static_cast<int>(band_end) - 1;
+    s.xout_abuf = static_cast<double*>(out_abuf);
+    s.xout_prog = static_cast<unsigned long long*>(out_prog);
+  }
+  std::vector<uint32_t> zero(1, 0);
+  if (int rc = run_sweeps(c, ps, zero, zero, zero, order, flags, o, st, s)) return rc;
+  unsigned long long key = ~0ull;
+  SK_CUDA(cudaMemcpyAsync(&key, c.err.p, sizeof key, cudaMemcpyDeviceToHost, c.stream()));
+  double v = std::numeric_limits<double>::quiet_NaN();
+  SK_CUDA(cudaMemcpyAsync(&v, c.values.p, sizeof v, cudaMemcpyDeviceToHost, c.stream()));
+  if (diag) SK_CUDA(cudaMemcpyAsync(diag, d_diag, nd * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  if (key != ~0ull) {
+    const auto xi = host_increments(x, lx, dim);
+    const auto yi = host_increments(y, ly, dim);
+    return decode_err(key, st, xi.data(), yi.data(), dim);
+  }
+  if (band_end == bands && value) *value = v;
+  return SK_OK;
+}
+
+// Single-GPU emulation of a two-strip pipeline: ONE launch sweeps every band
+// but routes the hand-off from band split-1 to band split through an
+// exchange buffer with system-scope release/acquire, exactly as two GPUs
+// would.  Used to test the strip path on one GPU (strips on one GPU may not
+// run as separate launches that wait on each other).
+int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
+                       size_t split_band, double* value, sk_status* st) {
+  clear_status(st);
+  size_t bands = 0;
+  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2 || split_band < 1 || split_band >= bands)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_split: split band outside (0, bands)");
+  void *xa = nullptr, *xp = nullptr;
+  if (int rc = sk_exchange_alloc(lx, order, &xa, &xp, st)) return rc;
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  const size_t ld = inc_ld(dim);
+  int rc = SK_OK;
+  do {
+    if (cudaError_t e = c.raw_x.ensure(lx * dim * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
+    if (cudaError_t e = c.raw_y.ensure(ly * dim * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
+    if (cudaError_t e = c.xinc.ensure(lx * ld * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
+    if (cudaError_t e = c.yinc.ensure(ly * ld * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
+    if (cudaError_t e = c.values.ensure(sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
+    if (cudaError_t e = c.err.ensure(sizeof(unsigned long long)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
+    cudaMemcpyAsync(c.raw_x.p, x, lx * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream());
+    cudaMemcpyAsync(c.raw_y.p, y, ly * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream());
+    launch_increments(c.raw_x.as<double>(), 1, lx, dim, ld, c.xinc.as<double>(), c.stream());
+    launch_increments(c.raw_y.as<double>(), 1, ly, dim, ld, c.yinc.as<double>(), c.stream());
+    cudaMemsetAsync(c.err.p, 0xff, sizeof(unsigned long long), c.stream());
+    cudaMemsetAsync(c.values.p, 0xff, sizeof(double), c.stream());
+    PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), lx * ld, ly * ld, static_cast<int>(ly - 1),
+               static_cast<int>(lx - 1), static_cast<int>(dim), static_cast<int>(ld)};
+    Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(), nullptr, nullptr, nullptr, 0, 0};
+    Strip s;
+    s.xin_band = static_cast<int>(split_band);
+    s.xout_band = static_cast<int>(split_band) - 1;
+    s.xin_abuf = static_cast<const double*>(xa);
+    s.xout_abuf = static_cast<double*>(xa);
+    s.xin_prog = static_cast<const unsigned long long*>(xp);
+    s.xout_prog = static_cast<unsigned long long*>(xp);
+    std::vector<uint32_t> zero(1, 0);
+    if ((rc = run_sweeps(c, ps, zero, zero, zero, order, flags, o, st, s)) != SK_OK) break;
+    unsigned long long key = ~0ull;
+    cudaMemcpyAsync(&key, c.err.p, sizeof key, cudaMemcpyDeviceToHost, c.stream());
+    cudaMemcpyAsync(value, c.values.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream());
+    if (cudaError_t e = cudaStreamSynchronize(c.stream()); e != cudaSuccess) { rc = cuda_fail(st, e, "sync"); break; }
+    if (key != ~0ull) rc = decode_err(key, st, nullptr, nullptr, dim);
+  } while (false);
+  sk_exchange_free(xa, xp);
+  return rc;
 }
 
 int sk_gram_shard_range(size_t m, size_t shard, size_t nshards, size_t* first, size_t* last) {

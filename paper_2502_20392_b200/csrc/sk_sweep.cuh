@@ -88,6 +88,17 @@ struct SweepParams {
   double* grid;                   // per output slot: lx x ly knot grid, or null
   double* diag;                   // per output slot: K at tiles (i, i), or null
   unsigned long long grid_stride, diag_stride;
+  // Band range of this launch ([0, bands) normally; a strip of a long pair on
+  // one GPU of a multi-GPU pipeline otherwise) and the cross-strip hand-off:
+  // band xout_band writes its alpha' to xout_abuf / publishes xout_prog
+  // (peer memory of the next GPU, system-scope release), band xin_band reads
+  // xin_abuf / waits on xin_prog (written by the previous GPU).  -1: none.
+  int band_begin, band_end;
+  int xin_band, xout_band;
+  const double* xin_abuf;
+  const unsigned long long* xin_prog;
+  double* xout_abuf;
+  unsigned long long* xout_prog;
 };
 
 constexpr unsigned kFlagStrictCorner = 1u;
@@ -120,7 +131,8 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // every other waiting warp then bails out too.
 static __device__ __noinline__ bool wait_progress_slow(const unsigned long long* ptr, unsigned long long need,
                                                        unsigned long long& seen, unsigned long long* wd,
-                                                       unsigned long long limit_ns, unsigned p, unsigned b) {
+                                                       unsigned long long limit_ns, unsigned p, unsigned b,
+                                                       bool sys) {
   // poll with relaxed loads (no L1 invalidation per poll) and a growing
   // back-off; the acquire is taken once the value is there
   const unsigned long long t0 = globaltimer_ns();
@@ -128,7 +140,7 @@ static __device__ __noinline__ bool wait_progress_slow(const unsigned long long*
   for (unsigned it = 1;; ++it) {
     __nanosleep(ns);
     if (ns < 1024) ns += ns >> 1;
-    if (ld_relaxed_gpu(ptr) >= need) break;
+    if ((sys ? ld_relaxed_sys(ptr) : ld_relaxed_gpu(ptr)) >= need) break;
     if ((it & 15) == 0) {
       if (*reinterpret_cast<volatile unsigned long long*>(wd) != 0) return false;
       if (globaltimer_ns() - t0 > limit_ns) {
@@ -136,26 +148,26 @@ static __device__ __noinline__ bool wait_progress_slow(const unsigned long long*
           wd[1] = p;
           wd[2] = b;
           wd[3] = need;
-          wd[4] = ld_relaxed_gpu(ptr);
+          wd[4] = sys ? ld_relaxed_sys(ptr) : ld_relaxed_gpu(ptr);
         }
         return false;
       }
     }
   }
-  seen = ld_acquire_gpu(ptr);
+  seen = sys ? ld_acquire_sys(ptr) : ld_acquire_gpu(ptr);
   return true;
 }
 
 __device__ __forceinline__ bool wait_progress(const SweepParams& P, const unsigned long long* ptr,
                                               unsigned long long need, unsigned long long& seen, unsigned p,
-                                              unsigned b) {
+                                              unsigned b, bool sys = false) {
   if (seen >= need) return true;
-  const unsigned long long v = ld_acquire_gpu(ptr);  // every lane polls the same word
+  const unsigned long long v = sys ? ld_acquire_sys(ptr) : ld_acquire_gpu(ptr);  // every lane polls one word
   if (v >= need) {
     seen = v;
     return true;
   }
-  return wait_progress_slow(ptr, need, seen, P.watchdog, P.watchdog_ns, p, b);
+  return wait_progress_slow(ptr, need, seen, P.watchdog, P.watchdog_ns, p, b, sys);
 }
 
 template <int NA>
@@ -218,6 +230,14 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   unsigned long long* prog_row = P.prog + static_cast<size_t>(slot) * P.bands;
   const bool has_below = b > 0;
   const bool has_above = b + 1 < static_cast<unsigned>(P.bands);
+  // where this band's alpha comes from / goes to: the pair's column buffer,
+  // or a cross-strip exchange buffer (multi-GPU long pair)
+  const bool xin = static_cast<int>(b) == P.xin_band;
+  const bool xout = static_cast<int>(b) == P.xout_band;
+  const double* in_buf = xin ? P.xin_abuf : colbuf;
+  const unsigned long long* in_prog = xin ? P.xin_prog : prog_row + (has_below ? b - 1 : 0);
+  double* out_buf = xout ? P.xout_abuf : colbuf;
+  unsigned long long* out_prog = xout ? P.xout_prog : prog_row + b;
   const unsigned out = P.pair_out[p];
   const bool strict = (P.flags & kFlagStrictCorner) != 0;
   const bool fault = (P.flags & kFlagWFault) != 0;
@@ -269,7 +289,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     const int col0 = g * K;
     const int ncol = max(0, min(K, cols - col0));
     if (has_below) {
-      const double* src = colbuf + static_cast<size_t>(col0) * NP;
+      const double* src = in_buf + static_cast<size_t>(col0) * NP;
       double* dst = s_alpha + (g & 1) * kStage;
       const int pieces = ncol * NP / 2;
       for (int k = lane; k < pieces; k += 32) cp_async_16(dst + 2 * k, src + 2 * k);
@@ -310,7 +330,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     for (int e = lane; e < (RING / 2) * XS; e += 32) s_ring[(RING / 2) * XS + e] = 0.0;
   }
   __syncwarp();
-  if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, K), seen, p, b)) return;
+  if (has_below && !wait_progress(P, in_prog, base + min(cols, K), seen, p, b, xin)) return;
   stage_group(0);
 
   // one step = R tiles of this lane (one basic block, conditional work predicated)
@@ -367,8 +387,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   for (int c0 = 0, chunk = 0; c0 < steps; c0 += K, ++chunk) {
     __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
     if (chunk + 1 < ngroups) {
-      if (has_below && !wait_progress(P, prog_row + (b - 1), base + min(cols, (chunk + 2) * K), seen, p, b))
-        return;
+      if (has_below && !wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin)) return;
       stage_group(chunk + 1);
       cp_async_wait<1>();
     } else {
@@ -462,16 +481,22 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
         const int jj = jfirst + kk;
         if (jj >= 0 && jj < cols) {
           const double2 v = *reinterpret_cast<const double2*>(s_out + 2 * e);
-          __stcg(reinterpret_cast<double2*>(colbuf + static_cast<size_t>(jj) * NP + (2 * e - kk * NP)), v);
+          __stcg(reinterpret_cast<double2*>(out_buf + static_cast<size_t>(jj) * NP + (2 * e - kk * NP)), v);
         }
       }
       // columns handed up before / after this chunk
       const int done0 = min(max(jfirst, 0), cols);
       const int done1 = min(max(jfirst + kend, 0), cols);
       if (done1 > done0 && (done1 == cols || done1 / kPublish != done0 / kPublish)) {
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_gpu(prog_row + b, base + done1);
+        if (xout) {
+          __threadfence_system();  // peer-memory data before the peer-visible counter
+          __syncwarp();
+          if (lane == 0) st_release_sys(out_prog, base + done1);
+        } else {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) st_release_gpu(out_prog, base + done1);
+        }
       }
     }
   }
@@ -502,8 +527,9 @@ __global__ void __launch_bounds__(kSweepWarps * 32, SK_MIN_BLOCKS) sweep_kernel(
   extern __shared__ __align__(16) double s_dyn[];
   double* smem = s_dyn + (threadIdx.x >> 5) * stage_doubles_per_warp(N, DP);
   const int lane = threadIdx.x & 31;
-  const unsigned total_units = static_cast<unsigned>(P.npairs) * static_cast<unsigned>(P.bands);
-  const unsigned gsz = static_cast<unsigned>(P.group) * static_cast<unsigned>(P.bands);
+  const unsigned nb = static_cast<unsigned>(P.band_end - P.band_begin);
+  const unsigned total_units = static_cast<unsigned>(P.npairs) * nb;
+  const unsigned gsz = static_cast<unsigned>(P.group) * nb;
   for (;;) {
     unsigned u = 0;
     if (lane == 0) u = atomicAdd(P.queue, 1u);
@@ -515,8 +541,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32, SK_MIN_BLOCKS) sweep_kernel(
     const unsigned rem = u - g * gsz;
     const unsigned g0 = g * static_cast<unsigned>(P.group);
     const unsigned gcount = min(static_cast<unsigned>(P.group), static_cast<unsigned>(P.npairs) - g0);
-    const unsigned b = rem / gcount;
-    const unsigned p = g0 + (rem - b * gcount);
+    const unsigned b = static_cast<unsigned>(P.band_begin) + rem / gcount;
+    const unsigned p = g0 + (rem - (b - static_cast<unsigned>(P.band_begin)) * gcount);
     sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem);
   }
 }

@@ -105,3 +105,118 @@ def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] 
     else:
         r.bound = math.nan
     return r
+
+
+# ------------------------------------------------------------ long pairs
+def strip_ranges(bands: int, world: int):
+    """Contiguous, balanced band ranges [b0, b1) of a long pair, one per rank."""
+    return [(bands * g // world, bands * (g + 1) // world) for g in range(world)]
+
+
+def first_error(records):
+    """The reference's 1-thread throw order (wavefront.cpp:133-173): among
+    per-strip first failures (code, tile_k, tile_l, message), the earliest
+    tile in (diagonal, row) order wins."""
+    best = None
+    for rec in records:
+        if rec is None:
+            continue
+        code, k, l, msg = rec
+        key = (k - 1 + l - 1, l - 1)
+        if best is None or key < best[0]:
+            best = (key, rec)
+    return None if best is None else best[1]
+
+
+def propagate_long_pair_distributed(x, y, order: int, options: Optional[sk.PropagateOptions] = None,
+                                    group=None, diag: bool = False):
+    """K(1,1) of ONE long pair split into row strips across the ranks of
+    `group` (one process per GPU): rank g sweeps a
+    contiguous band range and streams its top band's alpha series straight
+    into rank g+1's exchange buffer over NVLink (CUDA IPC peer mapping,
+    system-scope release/acquire).  Every rank returns (value, diag-or-None);
+    diag holds this rank's knots K(a, a) (NaN elsewhere)."""
+    import torch.distributed as dist
+
+    x, y = sk._as_series(x), sk._as_series(y)
+    if x.dim() != y.dim():
+        raise ValueError("propagate: series dimensions differ")
+    lib = _capi.load()
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    lx, ly, d = x.length(), y.length(), x.dim()
+    nb = ctypes.c_size_t()
+    if lib.sk_strip_bands(ly, int(order), ctypes.byref(nb)) != 0:
+        raise ValueError("propagate: bad length/order")
+    bands = nb.value
+    if bands < world:
+        raise ValueError(f"{bands} bands cannot feed {world} GPUs")
+    b0, b1 = strip_ranges(bands, world)[rank]
+    st = _capi.SkStatus()
+    in_a, in_p, out_a, out_p = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    handles = None
+    if rank > 0:
+        sk._check(lib.sk_exchange_alloc(lx, int(order), ctypes.byref(in_a), ctypes.byref(in_p), ctypes.byref(st)), st)
+        ha, hp = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
+        sk._check(lib.sk_ipc_handle(in_a, ha, ctypes.byref(st)), st)
+        sk._check(lib.sk_ipc_handle(in_p, hp, ctypes.byref(st)), st)
+        handles = (bytes(ha), bytes(hp))
+    all_handles = [None] * world
+    dist.all_gather_object(all_handles, handles, group=group)
+    try:
+        if rank + 1 < world:
+            ha, hp = all_handles[rank + 1]
+            sk._check(lib.sk_ipc_open(ctypes.create_string_buffer(ha, 64), ctypes.byref(out_a), ctypes.byref(st)), st)
+            sk._check(lib.sk_ipc_open(ctypes.create_string_buffer(hp, 64), ctypes.byref(out_p), ctypes.byref(st)), st)
+        dist.barrier(group=group)
+        value = ctypes.c_double(float("nan"))
+        dg = np.full(min(lx, ly) - 1, np.nan) if diag else None
+        xv, yv = x.values(), y.values()
+        rc = lib.sk_propagate_strip(sk._ptr(xv), lx, sk._ptr(yv), ly, d, int(order), sk._flags(options), b0, b1,
+                                    in_a if rank > 0 else None, in_p if rank > 0 else None,
+                                    out_a if rank + 1 < world else None, out_p if rank + 1 < world else None,
+                                    ctypes.byref(value), sk._ptr(dg) if dg is not None else None, ctypes.byref(st))
+        rec = None if rc == 0 else (int(st.code), int(st.tile_k), int(st.tile_l), st.message.decode(errors="replace"))
+        recs = [None] * world
+        dist.all_gather_object(recs, (rec, value.value if b1 == bands else None), group=group)
+    finally:
+        dist.barrier(group=group)
+        if rank + 1 < world:
+            if out_a.value:
+                lib.sk_ipc_close(out_a)
+            if out_p.value:
+                lib.sk_ipc_close(out_p)
+        if rank > 0:
+            lib.sk_exchange_free(in_a, in_p)
+    err = first_error([r for r, _ in recs])
+    if err is not None:
+        code, k, l, msg = err
+        if code == _capi.SK_NUMERIC_OVERFLOW:
+            raise sk.NumericOverflowError(msg, k, l)
+        if code == _capi.SK_INCONSISTENT_BOUNDARY:
+            raise sk.InconsistentBoundaryError(msg)
+        raise RuntimeError(msg)
+    final = [v for _, v in recs if v is not None][0]
+    return final, dg
+
+
+def propagate_split_emulated(x, y, order: int, split_band: int, options: Optional[sk.PropagateOptions] = None):
+    """One-GPU test of the strip protocol: a single launch whose hand-off from
+    band split_band-1 to split_band goes through an exchange buffer exactly
+    as between two GPUs (sk_propagate_split)."""
+    x, y = sk._as_series(x), sk._as_series(y)
+    lib = _capi.load()
+    st = _capi.SkStatus()
+    value = ctypes.c_double()
+    xv, yv = x.values(), y.values()
+    rc = lib.sk_propagate_split(sk._ptr(xv), x.length(), sk._ptr(yv), y.length(), x.dim(), int(order),
+                                sk._flags(options), int(split_band), ctypes.byref(value), ctypes.byref(st))
+    sk._check(rc, st)
+    return value.value
+
+
+def strip_bands(ly: int, order: int) -> int:
+    nb = ctypes.c_size_t()
+    if _capi.load().sk_strip_bands(ly, int(order), ctypes.byref(nb)) != 0:
+        raise ValueError("bad length/order")
+    return nb.value

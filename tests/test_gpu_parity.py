@@ -343,3 +343,18 @@ def test_gram_shards_reassemble(sk, restatement):
     vals = full.values.reshape(9, 9)
     assert np.array_equal(vals, vals.T)
     assert (np.diag(vals) >= 1.0 - 1e-10).all()
+
+
+# ------------------------------------------------------- multi-GPU strips
+def test_strip_protocol_emulated_on_one_gpu(sk, restatement):
+    """The long-pair strip hand-off (system-scope release/acquire through an
+    exchange buffer) inside one launch: bit-identical to the plain sweep."""
+    from paper_2502_20392_b200.distributed import propagate_split_emulated, strip_bands
+    x = restatement.brownian(300, 4, 5)
+    y = restatement.brownian(400, 4, 6)
+    for order in (8, 20):
+        plain = sk.propagate(x, y, order).value
+        nb = strip_bands(400, order)
+        assert nb >= 3
+        for split in range(1, nb):
+            assert propagate_split_emulated(x, y, order, split) == plain, (order, split)

@@ -198,3 +198,21 @@ def test_distributed_gram_assembly_gloo():
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(0, True), (1, True)]
+
+
+def test_strip_partition_and_error_order():
+    from paper_2502_20392_b200.distributed import first_error, strip_bands, strip_ranges
+    assert strip_bands(1_000_001, 8) == (1_000_000 + 31) // 32
+    for bands in (2, 7, 31250):
+        for world in (1, 2, 3, 8):
+            if bands < world:
+                continue
+            r = strip_ranges(bands, world)
+            assert r[0][0] == 0 and r[-1][1] == bands
+            assert all(r[g][1] == r[g + 1][0] and r[g][0] < r[g][1] for g in range(world - 1))
+    # earliest tile in (diagonal, row) order wins across strips
+    recs = [None, (2, 10, 40, "a"), (3, 30, 19, "b"), (2, 20, 30, "c")]
+    assert first_error(recs)[3] == "b"          # diagonal 47 < 48
+    recs = [(2, 10, 40, "a"), (2, 20, 30, "c")]  # same diagonal: lower row first
+    assert first_error(recs)[3] == "c"
+    assert first_error([None, None]) is None
