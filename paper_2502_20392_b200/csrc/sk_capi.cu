@@ -290,9 +290,13 @@ unsigned long long watchdog_ns() {
 }
 
 int check_watchdog(Ctx& c, sk_status* st) {
-  unsigned long long h[5] = {0, 0, 0, 0, 0};
+  unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   SK_CUDA(cudaMemcpyAsync(h, c.wd.p, sizeof h, cudaMemcpyDeviceToHost, c.stream()));
   SK_CUDA(cudaStreamSynchronize(c.stream()));
+#ifdef SK_PROFILE_WAITS
+  std::fprintf(stderr, "[sk] dependency waits: %.2f%% of band time (%.2f%% at band start)\n",
+               h[7] ? 100.0 * h[6] / h[7] : 0.0, h[7] ? 100.0 * h[5] / h[7] : 0.0);
+#endif
   if (h[0] == 0) return SK_OK;
   return set_status(st, SK_INTERNAL, 0, 0,
                     "sweep watchdog: dependency wait timed out (pair %llu band %llu needs %llu, saw %llu)", h[1], h[2],
@@ -349,6 +353,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     const int nb = (strip.band_end < 0 ? bands : strip.band_end) - strip.band_begin;
     const unsigned long long units = static_cast<unsigned long long>(npairs) * nb;
     int blocks = bps * c.sms;
+    if (const char* e = std::getenv("SK_FORCE_BPS")) blocks = std::max(1, std::min(bps, std::atoi(e))) * c.sms;
     const unsigned long long need_blocks = (units + kSweepWarps - 1) / kSweepWarps;
     if (static_cast<unsigned long long>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
     const size_t warps = static_cast<size_t>(blocks) * kSweepWarps;
@@ -418,6 +423,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.queue = c.queue.as<unsigned>();
     P.watchdog = c.wd.as<unsigned long long>();
     P.watchdog_ns = watchdog_ns();
+    // with fewer pairs than warps, ~warps/group bands of each pair run at
+    // once; their natural spacing is one band time / (warps / group)
+    P.start_lag = group < warps ? static_cast<int>(0.75 * (cols + 32.0) * group / warps) : 0;
+    if (const char* e = std::getenv("SK_START_LAG")) P.start_lag = std::atoi(e);
     P.values = o.d_values;
     P.err = o.d_err;
     P.maxrho = o.d_maxrho;

@@ -82,6 +82,7 @@ struct SweepParams {
   unsigned* queue;                // unit counter
   unsigned long long* watchdog;   // [0] abort flag, [1..4] first stuck wait (p, b, need, seen)
   unsigned long long watchdog_ns; // give up a dependency wait after this long
+  int start_lag;                  // columns the band below must be ahead before a band starts
   double* values;                 // per output slot: K(1,1)
   unsigned long long* err;        // per output slot: min error key (init ~0)
   unsigned long long* maxrho;     // per output slot: max |delta| bits (init 0) or null
@@ -129,6 +130,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // scheduling bug -- by construction every awaited unit is running) records
 // itself, raises the abort flag and returns false instead of hanging the GPU;
 // every other waiting warp then bails out too.
+#ifdef SK_PROFILE_WAITS
+// per-unit trace (diagnostic build only): {p | b << 20 | smid << 40, start ns, end ns, wait ns}
+constexpr unsigned kTraceUnits = 1u << 16;
+__device__ unsigned long long g_utrace[kTraceUnits * 4];
+__device__ unsigned long long g_wwait[1u << 14];
+#endif
+
 static __device__ __noinline__ bool wait_progress_slow(const unsigned long long* ptr, unsigned long long need,
                                                        unsigned long long& seen, unsigned long long* wd,
                                                        unsigned long long limit_ns, unsigned p, unsigned b,
@@ -167,7 +175,21 @@ __device__ __forceinline__ bool wait_progress(const SweepParams& P, const unsign
     seen = v;
     return true;
   }
+#ifdef SK_PROFILE_WAITS
+  const long long t0 = clock64();
+  const unsigned long long g0 = globaltimer_ns();
+  const bool ok = wait_progress_slow(ptr, need, seen, P.watchdog, P.watchdog_ns, p, b, sys);
+  if ((threadIdx.x & 31) == 0) {
+    g_wwait[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] += globaltimer_ns() - g0;
+    atomicAdd(reinterpret_cast<unsigned long long*>(P.watchdog + 6), clock64() - t0);
+    // [5]: cycles of waits whose target is the band's first chunks (start-up lag)
+    if (need - static_cast<unsigned long long>(p) * (P.cols + 1) <= max(64, P.start_lag))
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.watchdog + 5), clock64() - t0);
+  }
+  return ok;
+#else
   return wait_progress_slow(ptr, need, seen, P.watchdog, P.watchdog_ns, p, b, sys);
+#endif
 }
 
 template <int NA>
@@ -279,6 +301,22 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   unsigned jkey[R];  // (first failing column << 2) | code, per tile
 #pragma unroll
   for (int r = 0; r < R; ++r) jkey[r] = ~0u;
+  // the rows' increments stay in registers for the whole band: a reload per
+  // chunk would miss L1, which every acquire of the progress counter invalidates
+  double dyr[R][DP > 0 ? DP : 1];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if constexpr (DP > 0) {
+#pragma unroll
+      for (int c = 0; c < DP; c += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(yrow[r] + c));
+        dyr[r][c] = v.x;
+        dyr[r][c + 1] = v.y;
+      }
+    } else {
+      dyr[r][0] = 0.0;
+    }
+  }
   unsigned long long seen = 0;
   const int steps = cols + rb - 1;
 
@@ -330,7 +368,10 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     for (int e = lane; e < (RING / 2) * XS; e += 32) s_ring[(RING / 2) * XS + e] = 0.0;
   }
   __syncwarp();
-  if (has_below && !wait_progress(P, in_prog, base + min(cols, K), seen, p, b, xin)) return;
+  // start no closer than start_lag columns behind the band below: bands of
+  // one pair then run evenly spread in time instead of bunched at the
+  // minimum hand-over distance, where every timing jitter becomes a wait
+  if (has_below && !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin)) return;
   stage_group(0);
 
   // one step = R tiles of this lane (one basic block, conditional work predicated)
@@ -369,7 +410,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
                             : !isfinite(total)                               ? kErrNonFinite
                                                                              : 0u;
       const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
-      jkey[r] = (active && code != 0u && kk < jkey[r]) ? kk : jkey[r];
+      jkey[r] = min(jkey[r], (active && code != 0u) ? kk : ~0u);
       st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
       if constexpr (EXTRAS) {
         if (P.grid)
@@ -401,15 +442,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     // c0 + k - t - 32 r) with the delta guard (wavefront.cpp:150-155) and max|delta|
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      double dy[DP > 0 ? DP : 1];
-      if constexpr (DP > 0) {
-#pragma unroll
-        for (int c = 0; c < DP; c += 2) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(yrow[r] + c));
-          dy[c] = v.x;
-          dy[c + 1] = v.y;
-        }
-      }
+      const double (&dy)[DP > 0 ? DP : 1] = dyr[r];
 #pragma unroll 1
       for (int k0 = 0; k0 < K; k0 += 4) {
         double dd[4];
@@ -453,7 +486,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
           const double ad = fabs(dd[u]);
           if constexpr (EXACT) mx = fmax(mx, act ? ad : 0.0);
           const unsigned kk = (static_cast<unsigned>(j) << 2) | kErrDelta;
-          jkey[r] = (act && !(ad <= kDeltaOverflowLimit) && kk < jkey[r]) ? kk : jkey[r];
+          jkey[r] = min(jkey[r], (act && !(ad <= kDeltaOverflowLimit)) ? kk : ~0u);
         }
       }
     }
@@ -488,14 +521,16 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
       const int done0 = min(max(jfirst, 0), cols);
       const int done1 = min(max(jfirst + kend, 0), cols);
       if (done1 > done0 && (done1 == cols || done1 / kPublish != done0 / kPublish)) {
-        if (xout) {
-          __threadfence_system();  // peer-memory data before the peer-visible counter
-          __syncwarp();
-          if (lane == 0) st_release_sys(out_prog, base + done1);
-        } else {
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) st_release_gpu(out_prog, base + done1);
+        // bar.warp.sync orders every lane's column stores before lane 0's
+        // release store (PTX memory model: barrier synchronisation is part
+        // of causality order), so one release by one lane publishes them all
+        // -- no per-lane fence.sc (MEMBAR.SC + L1 invalidation)
+        __syncwarp();
+        if (lane == 0) {
+          if (xout)
+            st_release_sys(out_prog, base + done1);  // peer-memory data before the peer-visible counter
+          else
+            st_release_gpu(out_prog, base + done1);
         }
       }
     }
@@ -543,7 +578,26 @@ __global__ void __launch_bounds__(kSweepWarps * 32, SK_MIN_BLOCKS) sweep_kernel(
     const unsigned gcount = min(static_cast<unsigned>(P.group), static_cast<unsigned>(P.npairs) - g0);
     const unsigned b = static_cast<unsigned>(P.band_begin) + rem / gcount;
     const unsigned p = g0 + (rem - (b - static_cast<unsigned>(P.band_begin)) * gcount);
+#ifdef SK_PROFILE_WAITS
+    const long long t0 = clock64();
+    const unsigned long long gt0 = globaltimer_ns();
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0) g_wwait[wid] = 0;
     sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem);
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.watchdog + 7), clock64() - t0);
+      if (u < kTraceUnits) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_utrace[4 * u] = p | (static_cast<unsigned long long>(b) << 20) | (static_cast<unsigned long long>(smid) << 40);
+        g_utrace[4 * u + 1] = gt0;
+        g_utrace[4 * u + 2] = globaltimer_ns();
+        g_utrace[4 * u + 3] = g_wwait[wid];
+      }
+    }
+#else
+    sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem);
+#endif
   }
 }
 

@@ -2,6 +2,10 @@
 // (Makefile) so the 17 x 5 x 2 sweep instantiations build in parallel.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "sk_sweep.cuh"
 
 #ifndef SK_N
@@ -29,6 +33,17 @@ static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& 
   cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
   if (e != cudaSuccess) return e;
   sweep_kernel<N, DP, EXACT, EXTRAS><<<grid, kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>(), stream>>>(P);
+#ifdef SK_PROFILE_WAITS
+  if (const char* path = std::getenv("SK_UTRACE")) {
+    static std::vector<unsigned long long> h(kTraceUnits * 4);
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h.data(), g_utrace, h.size() * sizeof(unsigned long long));
+    if (FILE* f = std::fopen(path, "wb")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
+#endif
   return cudaGetLastError();
 }
 
