@@ -45,9 +45,13 @@ __device__ __forceinline__ unsigned long long err_key(unsigned i, unsigned j, un
 }
 
 // tile_series.cpp:70-75
+// |a0 - b0| > 1e-9 max(1, |a0|, |b0|), as three comparisons: scaling by a
+// positive constant is monotone under rounding, so this is the same
+// predicate (NaN operands compare false in both forms), without the
+// fmax select chains and branches
 __device__ __forceinline__ bool corner_mismatch(double a0, double b0) {
-  const double scale = fmax(1.0, fmax(fabs(a0), fabs(b0)));
-  return fabs(a0 - b0) > 1e-9 * scale;
+  const double d = fabs(a0 - b0);
+  return (d > 1e-9) & (d > 1e-9 * fabs(a0)) & (d > 1e-9 * fabs(b0));
 }
 
 // Sequential non-FMA dot product in coordinate order: bit-identical to

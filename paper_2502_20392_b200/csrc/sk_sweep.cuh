@@ -45,9 +45,16 @@ constexpr int kPublish = 32;      // columns per progress publication
 // Warps per CTA.  Warps are fully independent; one-warp CTAs avoid losing
 // residency to CTA-granular register allocation.
 constexpr int kSweepWarps = SK_SWEEP_WARPS;
+// Resident one-warp CTAs per SM the register allocation must allow: each
+// SM sub-partition holds 16K registers, so <= 168 registers/thread gives 3
+// warps per sub-partition (12 per SM), more gives only 2.  Orders up to 10
+// fit 168 without spills; larger orders keep the unconstrained allocation.
 #ifndef SK_MIN_BLOCKS
-#define SK_MIN_BLOCKS 1
+#define SK_MIN_BLOCKS 0
 #endif
+__host__ __device__ constexpr int sweep_min_blocks(int N) {
+  return SK_MIN_BLOCKS > 0 ? SK_MIN_BLOCKS : (N >= 1 && N <= 10 ? 12 : 1);
+}
 
 // Rows per lane.  R = 2: a warp sweeps a 64-row band, lane t owning rows t
 // and t + 32 (the second tile 32 columns behind the first), so two
@@ -406,9 +413,9 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
       // the reference's throw order inside a tile: delta guard (checked when
       // the chunk's deltas are formed), corner check, non-finite total
       // (wavefront.cpp:150-173); the first failing tile of the row wins
-      const unsigned code = (strict && corner_mismatch(q[r][0], r_in[r][0])) ? kErrCorner
-                            : !isfinite(total)                               ? kErrNonFinite
-                                                                             : 0u;
+      const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0]);
+      const bool nf = !isfinite(total);
+      const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
       const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
       jkey[r] = min(jkey[r], (active && code != 0u) ? kk : ~0u);
       st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
@@ -558,7 +565,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
 // Persistent: grid = resident CTAs; dynamic shared memory =
 // kSweepWarps * stage_doubles_per_warp(N, DP) doubles.
 template <int N, int DP, bool EXACT, bool EXTRAS>
-__global__ void __launch_bounds__(kSweepWarps * 32, SK_MIN_BLOCKS) sweep_kernel(const SweepParams P) {
+__global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_kernel(const SweepParams P) {
   extern __shared__ __align__(16) double s_dyn[];
   double* smem = s_dyn + (threadIdx.x >> 5) * stage_doubles_per_warp(N, DP);
   const int lane = threadIdx.x & 31;
@@ -587,8 +594,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32, SK_MIN_BLOCKS) sweep_kernel(
     if (lane == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(P.watchdog + 7), clock64() - t0);
       if (u < kTraceUnits) {
-        unsigned smid;
+        unsigned smid, hwwarp;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(hwwarp));
+        smid |= hwwarp << 8;
         g_utrace[4 * u] = p | (static_cast<unsigned long long>(b) << 20) | (static_cast<unsigned long long>(smid) << 40);
         g_utrace[4 * u + 1] = gt0;
         g_utrace[4 * u + 2] = globaltimer_ns();

@@ -22,10 +22,16 @@ static size_t smem_bytes() {
 template <int N, int DP, bool EXACT, bool EXTRAS>
 static cudaError_t prepare() {
   const size_t smem = smem_bytes<N, DP, EXACT, EXTRAS>();
-  if (smem > 48 * 1024)
-    return cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem));
-  return cudaSuccess;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  // the whole unified L1/shared array as shared memory: residency is set by
+  // registers and the per-warp stage, never by a smaller default carveout
+  // (the sweep reads global memory only through L2-bypassing cp.async)
+  return cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              cudaSharedmemCarveoutMaxShared);
 }
 
 template <int N, int DP, bool EXACT, bool EXTRAS>

@@ -90,6 +90,31 @@ __global__ void reg_const(double* out, int iters) {
   if (s == 1.2345) out[0] = s;
 }
 
+// conv pattern: acc[c] = fma(x[c], pv, acc[c]) with pv a per-lane register
+// shared by 8 consecutive DFMAs (operand reuse cache), 3 register operands
+__global__ void shared_reg(double* out, int iters) {
+  double acc[8], x[8];
+  double pv = 1.0 + threadIdx.x * 1e-13, pw = 1.0 - threadIdx.x * 1e-13;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    acc[c] = threadIdx.x + c;
+    x[c] = 1.0 + 1e-9 * c;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma(x[c], pv, acc[c]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = fma(acc[c], pw, x[c]);
+    const double t = pv;
+    pv = pw;
+    pw = t;
+  }
+  double s = pv + pw;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c] + x[c];
+  if (s == 1.2345) out[0] = s;
+}
+
 template <class F>
 void run(const char* name, F launch, double flops_per_launch) {
   cudaEvent_t e0, e1;
@@ -116,6 +141,7 @@ int main() {
   run("distinct3", [&] { distinct3<<<blocks, tpb>>>(out, iters); }, fl);
   run("reg_const", [&] { reg_const<<<blocks, tpb>>>(out, iters); }, fl);
   run("const_operand", [&] { const_operand<<<blocks, tpb>>>(out, iters); }, fl);
+  run("shared_reg", [&] { shared_reg<<<blocks, tpb>>>(out, iters); }, fl);
   run("shared_operand", [&] { shared_operand<<<blocks, tpb>>>(out, iters, 1.0000001); }, fl);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 from paper_2502_20392_b200 import _capi, sigker as sk  # noqa: E402
 
 
-def run(npairs, lx, ly, dim, order, reps=3):
+def run(npairs, lx, ly, dim, order, reps=3, flags=_capi.SK_STRICT_CORNER):
     rng = np.random.default_rng(0)
     xs = np.cumsum(rng.standard_normal((npairs, lx, dim)) / np.sqrt(lx), axis=1)
     ys = np.cumsum(rng.standard_normal((npairs, ly, dim)) / np.sqrt(ly), axis=1)
@@ -24,7 +24,7 @@ def run(npairs, lx, ly, dim, order, reps=3):
     lib.sk_set_stream(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ctypes.byref(st))
     def once():
         rc = lib.sk_pairwise_device(ctypes.c_void_p(xd.data_ptr()), lx, ctypes.c_void_p(yd.data_ptr()), ly, npairs,
-                                    dim, 0, order, 1e-12, 0, ctypes.c_void_p(vd.data_ptr()), None, None, None,
+                                    dim, 0, order, 1e-12, flags, ctypes.c_void_p(vd.data_ptr()), None, None, None,
                                     ctypes.byref(st))
         assert rc == 0, st.message
     once()
@@ -44,6 +44,7 @@ def run(npairs, lx, ly, dim, order, reps=3):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("shapes", nargs="*", default=["256,4096,4096,8,8"])
+    ap.add_argument("--no-strict", action="store_true", help="skip the per-tile corner check (bench uses it)")
     a = ap.parse_args()
     for sh in a.shapes:
-        run(*[int(v) for v in sh.split(",")])
+        run(*[int(v) for v in sh.split(",")], flags=0 if a.no_strict else _capi.SK_STRICT_CORNER)
