@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -182,6 +183,11 @@ struct Ctx {
       scan, wd;
   bool stats_on = false;
   std::vector<StatRec> stats;
+  // host-side caches: cudaMemGetInfo can take milliseconds (driver round
+  // trip), occupancy queries are per kernel variant and never change
+  size_t free_cache = 0;
+  int free_age = 0;
+  std::map<int, int> occupancy;
   uint64_t sweep_launches = 0, aux_launches = 0, table_launches = 0;
   double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0, done_table_ms = 0.0;
 
@@ -331,11 +337,23 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   int bps = 0;
   const bool exact = o.d_maxrho != nullptr;
   const bool extras = o.d_grid != nullptr || o.d_diag != nullptr;
-  SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, &bps));
+  const int okey = ((ntempl * 32 + dp) * 2 + (exact ? 1 : 0)) * 2 + (extras ? 1 : 0);
+  if (auto it = c.occupancy.find(okey); it != c.occupancy.end()) {
+    bps = it->second;
+  } else {
+    SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, &bps));
+    c.occupancy[okey] = bps;
+  }
   if (bps < 1) return set_status(st, SK_CUDA_ERROR, 0, 0, "sweep kernel cannot be resident (occupancy 0)");
   Tracer tr;
-  size_t free_b = 0, total_b = 0;
-  SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  // free device memory for the workspace budgets below, refreshed every 32
+  // launches (a heuristic input; allocation failures still surface)
+  if (c.free_cache == 0 || ++c.free_age > 32) {
+    size_t total_b = 0;
+    SK_CUDA(cudaMemGetInfo(&c.free_cache, &total_b));
+    c.free_age = 0;
+  }
+  const size_t free_b = c.free_cache;
   tr.mark("  occupancy+memgetinfo");
 
   // large d: per-pair rho tables (rows x cols), pairs chunked to a memory budget

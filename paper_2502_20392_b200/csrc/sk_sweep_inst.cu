@@ -2,6 +2,7 @@
 // (Makefile) so the 17 x 5 x 2 sweep instantiations build in parallel.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -21,17 +22,26 @@ static size_t smem_bytes() {
 
 template <int N, int DP, bool EXACT, bool EXTRAS>
 static cudaError_t prepare() {
+  // function attributes are per device: set them once per device
+  static std::atomic<unsigned long long> done_mask{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
   const size_t smem = smem_bytes<N, DP, EXACT, EXTRAS>();
   if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   // the whole unified L1/shared array as shared memory: residency is set by
   // registers and the per-warp stage, never by a smaller default carveout
   // (the sweep reads global memory only through L2-bypassing cp.async)
-  return cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                              cudaSharedmemCarveoutMaxShared);
+  e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 template <int N, int DP, bool EXACT, bool EXTRAS>
