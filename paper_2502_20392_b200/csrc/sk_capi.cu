@@ -180,7 +180,7 @@ struct Ctx {
   cudaStream_t user = nullptr;
   int sms = 148;
   DevBuf raw_x, raw_y, xinc, yinc, sqn, pairs, values, err, maxr, prog, queue, abuf, tab, grid, diag, w65, tile_io,
-      scan, wd;
+      scan, wd, susp, dep, rq;
   bool stats_on = false;
   std::vector<StatRec> stats;
   // host-side caches: cudaMemGetInfo can take milliseconds (driver round
@@ -198,7 +198,8 @@ struct Ctx {
       cudaEventDestroy(r.b);
     }
     DevBuf* all[] = {&raw_x, &raw_y, &xinc, &yinc, &sqn, &pairs, &values, &err, &maxr,
-                     &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan, &wd};
+                     &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan, &wd,
+                     &susp,  &dep,   &rq};
     for (DevBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
   }
@@ -366,6 +367,27 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // units per launch must fit 32 bits
   chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / bands));
 
+  // Segment-DAG geometry (SweepParams::seg_cols): used when the launch sweeps
+  // whole pairs with several units per warp; streaming otherwise (a
+  // latency-bound single short pair, multi-GPU strips).
+  const bool whole = strip.band_begin == 0 && strip.band_end < 0 && strip.xin_band < 0 && strip.xout_band < 0;
+  int seg_cols = 0;
+  unsigned spb = 0, units_pair = 0;
+  if (bands > 1 && whole && std::getenv("SK_STREAM") == nullptr) {
+    seg_cols = 256;  // B200, N = 8: 256 x 4096^2 62.1 % of the FP64 roof (128: 62.1, 512: 59.1, streaming 57.1)
+    if (const char* e = std::getenv("SK_SEG_COLS")) seg_cols = std::atoi(e);
+    seg_cols = std::max(band_rows, (seg_cols + band_rows - 1) / band_rows * band_rows);  // multiple of K and H
+    for (int b = 0; b < bands; ++b) {
+      const SegRange r = seg_range(rows, cols, b, band_rows, seg_cols);
+      spb = std::max<unsigned>(spb, static_cast<unsigned>(r.hi - r.lo + 1));
+      units_pair += static_cast<unsigned>(r.hi - r.lo + 1);
+    }
+    // the ready list holds every unit of a launch: at most 2^26 (256 MB)
+    if (units_pair > (1u << 26)) seg_cols = 0;
+    else chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 26) / units_pair));
+    chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / (static_cast<size_t>(bands) * spb)));
+  }
+
   for (size_t c0 = 0; c0 < npairs_all; c0 += chunk) {
     const size_t npairs = std::min(chunk, npairs_all - c0);
     const int nb = (strip.band_end < 0 ? bands : strip.band_end) - strip.band_begin;
@@ -398,11 +420,32 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     SK_CUDA(cudaMemcpyAsync(d_po, pout.data() + c0, npairs * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
     SK_CUDA(c.prog.ensure(slots * bands * sizeof(unsigned long long)));
     SK_CUDA(cudaMemsetAsync(c.prog.p, 0, slots * bands * sizeof(unsigned long long), c.stream()));
-    SK_CUDA(c.queue.ensure(sizeof(unsigned)));
-    SK_CUDA(cudaMemsetAsync(c.queue.p, 0, sizeof(unsigned), c.stream()));
+    // [0] static unit order; SweepParams::ctr at +kCtrLine (one 128-byte line per counter)
+    SK_CUDA(c.queue.ensure(4 * kCtrLine * sizeof(unsigned)));
+    SK_CUDA(cudaMemsetAsync(c.queue.p, 0, 4 * kCtrLine * sizeof(unsigned), c.stream()));
     SK_CUDA(c.wd.ensure(8 * sizeof(unsigned long long)));
     SK_CUDA(cudaMemsetAsync(c.wd.p, 0, 8 * sizeof(unsigned long long), c.stream()));
     if (bands > 1) SK_CUDA(c.abuf.ensure(slots * col_bytes));
+    // segment mode only with several units per warp (SK_FORCE_SEGMENTS: always, for tests)
+    const int seg_here = (units >= 4ull * warps || std::getenv("SK_FORCE_SEGMENTS") != nullptr) ? seg_cols : 0;
+    if (seg_here > 0) {
+      const size_t nrec = slots * static_cast<size_t>(bands);
+      SK_CUDA(c.susp.ensure(nrec * static_cast<size_t>(susp_record_doubles(ntempl)) * sizeof(double)));
+      SK_CUDA(c.dep.ensure(nrec * spb * sizeof(unsigned)));
+      SK_CUDA(cudaMemsetAsync(c.dep.p, 0, nrec * spb * sizeof(unsigned), c.stream()));
+      const size_t ncell = npairs * static_cast<size_t>(units_pair);
+      SK_CUDA(c.rq.ensure(ncell * sizeof(unsigned)));
+      SK_CUDA(cudaMemsetAsync(c.rq.p, 0, ncell * sizeof(unsigned), c.stream()));
+      // the first unit of each slot's first pair is ready
+      const unsigned first = static_cast<unsigned>(std::min(slots, npairs));
+      std::vector<unsigned> init(first + 1);
+      for (unsigned k = 0; k < first; ++k) init[k] = k * static_cast<unsigned>(bands) * spb + 1u;
+      SK_CUDA(cudaMemcpyAsync(c.rq.p, init.data(), first * sizeof(unsigned), cudaMemcpyHostToDevice, c.stream()));
+      init[first] = first;
+      SK_CUDA(cudaMemcpyAsync(c.queue.as<unsigned>() + 2 * kCtrLine, &init[first], sizeof(unsigned),
+                              cudaMemcpyHostToDevice, c.stream()));
+      SK_CUDA(cudaStreamSynchronize(c.stream()));  // `init` is pageable host memory
+    }
     if (dp == 0) {
       SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
       // exact (sequential) deltas when max|rho| is reported or the literal
@@ -460,6 +503,13 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.xin_prog = strip.xin_prog;
     P.xout_abuf = strip.xout_abuf;
     P.xout_prog = strip.xout_prog;
+    P.seg_cols = seg_here;
+    P.segs_per_band = static_cast<int>(spb);
+    P.units_total = static_cast<unsigned>(npairs) * units_pair;
+    P.susp = seg_here ? c.susp.as<double>() : nullptr;
+    P.dep = seg_here ? c.dep.as<unsigned>() : nullptr;
+    P.rq = seg_here ? c.rq.as<unsigned>() : nullptr;
+    P.ctr = c.queue.as<unsigned>() + kCtrLine;
 
     StatRec rec{};
     rec.tiles = static_cast<double>(npairs) * rows * cols;

@@ -107,7 +107,41 @@ struct SweepParams {
   const unsigned long long* xin_prog;
   double* xout_abuf;
   unsigned long long* xout_prog;
+  // Segment-DAG mode (seg_cols > 0): the unit is (pair, band, segment), a
+  // run of seg_cols steps of one band.  Band b's segment s covers steps
+  // [s L - b H, (s+1) L - b H) (L = seg_cols, H = rows per band), so the
+  // band below has produced every alpha a segment reads once its own segment
+  // s is done: a unit runs only when both inputs -- (b, s-1) and (b-1, s) --
+  // are complete and never waits inside.  Units become ready through
+  // dependency counters (dep, per slot x band x segment) and a ready ring
+  // (rq); bands carry their lane state between segments in susp records.
+  int seg_cols, segs_per_band;
+  unsigned units_total;
+  double* susp;
+  unsigned* dep;
+  unsigned* rq;   // ready list, units_total cells
+  unsigned* ctr;  // one 128-byte line each: [0] ready head, [kCtrLine] tail
 };
+
+constexpr int kCtrLine = 32;  // u32 words per counter line
+
+// sweep_band outcomes
+constexpr int kBandDone = 0, kBandAbort = 2;
+
+__host__ __device__ constexpr int susp_record_doubles(int N) {
+  return 32 * rows_per_lane(N) * (((N > 0 ? N + 1 : kMaxOrder + 1) + 1) & ~1) * 2;
+}
+
+// segment geometry of band b (rows per band H = 32 R)
+struct SegRange {
+  int lo, hi;  // first / last segment index of the band
+};
+__host__ __device__ inline int band_steps(int rows, int cols, int b, int H) {
+  return cols + min(H, rows - b * H) - 1;
+}
+__host__ __device__ inline SegRange seg_range(int rows, int cols, int b, int H, int L) {
+  return {b * H / L, (band_steps(rows, cols, b, H) - 1 + b * H) / L};
+}
 
 constexpr unsigned kFlagStrictCorner = 1u;
 constexpr unsigned kFlagWFault = 4u;
@@ -142,6 +176,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 constexpr unsigned kTraceUnits = 1u << 16;
 __device__ unsigned long long g_utrace[kTraceUnits * 4];
 __device__ unsigned long long g_wwait[1u << 14];
+__device__ unsigned g_tidx;
 #endif
 
 static __device__ __noinline__ bool wait_progress_slow(const unsigned long long* ptr, unsigned long long need,
@@ -199,6 +234,23 @@ __device__ __forceinline__ bool wait_progress(const SweepParams& P, const unsign
 #endif
 }
 
+// ---- ready list (segment-DAG mode, lane 0 only) ------------------------------
+// Every unit is pushed exactly once (the initial ones by the host), so the
+// list has units_total cells and never wraps: push takes the next cell with
+// the tail counter and publishes the unit (+1) with a release store; pop
+// takes the next cell with the head counter (always succeeds) and waits for
+// its unit.  A warp whose cell index is past the end has nothing left to do.
+__device__ __forceinline__ void rq_push(const SweepParams& P, unsigned unit) {
+  const unsigned t = atomicAdd(P.ctr + kCtrLine, 1u);
+  st_release_u32(P.rq + t, unit + 1u);
+}
+// one input of unit (slot-local index `di`, launch unit id `unit`) is
+// complete; the last of its `ndep` inputs queues it.  acq_rel: the unit's
+// runner sees every predecessor's stores.
+__device__ __forceinline__ void dep_arrive(const SweepParams& P, size_t di, unsigned ndep, unsigned unit) {
+  if (atom_add_acq_rel_u32(P.dep + di, 1u) + 1u == ndep) rq_push(P, unit);
+}
+
 template <int NA>
 __device__ __forceinline__ void lds_series(const double* src, double (&v)[NA], int n) {
 #pragma unroll
@@ -234,9 +286,15 @@ __device__ __forceinline__ void sts_series(double* dst, const double (&v)[NA], i
 // EXACT: delta by the reference's sequential non-FMA dot (bit-identical) and
 // per-pair max|delta| tracking (needed when the caller asks for max|rho|).
 // EXTRAS: knot-grid / diagonal outputs (propagate_grid, prefix knots).
+// Steps [c_begin K, min(c_end K, steps)) of band b of pair p.  Streaming
+// mode (P.seg_cols == 0): the whole band (c_begin = 0, c_end = INT_MAX),
+// waiting on the band below's progress counter.  Segment mode: one segment,
+// all inputs complete; `restore` loads the band's lane state from its record
+// (not the band's first segment), `save` stores it (not the last).
 template <int N, int DP, bool EXACT, bool EXTRAS>
-__device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, unsigned b, int lane,
-                                           double* __restrict__ smem) {
+__device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsigned b, int lane,
+                                          double* __restrict__ smem, int c_begin, int c_end, bool restore,
+                                          bool save) {
   constexpr int R = rows_per_lane(N);
   constexpr int K = chunk_cols(R);
   constexpr int RING = ring_rows(R);
@@ -270,14 +328,19 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
   const unsigned out = P.pair_out[p];
   const bool strict = (P.flags & kFlagStrictCorner) != 0;
   const bool fault = (P.flags & kFlagWFault) != 0;
+  const bool streaming = P.seg_cols == 0;
+  double* const rec = streaming ? nullptr
+                                : P.susp + (static_cast<size_t>(slot) * P.bands + b) *
+                                               static_cast<size_t>(susp_record_doubles(N));
 
   // Slot hand-over: band 0 of pair p rewrites the column buffer that the last
-  // band of the slot's previous pair (p - slots) reads.
-  if (b == 0 && has_above && p >= static_cast<unsigned>(P.slots)) {
+  // band of the slot's previous pair (p - slots) reads.  (Segment mode: the
+  // pair's first unit is queued only once the previous pair has finished.)
+  if (streaming && b == 0 && has_above && p >= static_cast<unsigned>(P.slots)) {
     unsigned long long seen0 = 0;
     if (!wait_progress(P, prog_row + (P.bands - 1),
                        static_cast<unsigned long long>(p - P.slots) * (cols + 1) + cols, seen0, p, b))
-      return;
+      return kBandAbort;
   }
 
   // per tile r of this lane: row i_r = row0 + 32 r + lane, column s - lane - 32 r
@@ -369,17 +432,43 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
     // band 0: the bottom edge of the domain is the unit series in every column
     for (int e = lane; e < 2 * kStage; e += 32) s_alpha[e] = (e % NP == 0) ? 1.0 : 0.0;
   }
-  for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
+  if (restore) {
+    // lane state at the segment boundary: beta (registers) and the
+    // lane-to-lane alpha slots
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < NA; ++m)
+        if (NA <= kMaxRegOrder + 1 || m < n) roA[r][m] = rec[(r * NP + m) * 32 + lane];
+    for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = rec[32 * R * NP + e];
+  } else {
+    for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
+  }
   if constexpr (DP > 0) {
-    // columns -RING/2..-1 (ring rows RING/2..RING-1): zero increments => delta = 0
-    for (int e = lane; e < (RING / 2) * XS; e += 32) s_ring[(RING / 2) * XS + e] = 0.0;
+    // dx of the columns the lanes still need behind the first staged group,
+    // [c K - 32 R, c K): zero below column 0 (zero increments => delta = 0,
+    // which keeps a tile's beta at the unit series before its first column)
+    const int h0 = c_begin * K - 32 * R;
+    for (int e = lane; e < 32 * R * (DP / 2); e += 32) {
+      const int c = e / (DP / 2), part = e - c * (DP / 2);
+      const int col = h0 + c;
+      double* dst = s_ring + (col & (RING - 1)) * XS + 2 * part;
+      if (col < 0) {
+        dst[0] = 0.0;
+        dst[1] = 0.0;
+      } else if (col < cols) {
+        cp_async_16(dst, xser + static_cast<size_t>(col) * DP + 2 * part);
+      }
+    }
   }
   __syncwarp();
   // start no closer than start_lag columns behind the band below: bands of
   // one pair then run evenly spread in time instead of bunched at the
   // minimum hand-over distance, where every timing jitter becomes a wait
-  if (has_below && !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin)) return;
-  stage_group(0);
+  if (streaming && has_below &&
+      !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin))
+    return kBandAbort;
+  stage_group(c_begin);
 
   // one step = R tiles of this lane (one basic block, conditional work predicated)
   auto step = [&](int s, int k, const double* stage, const double* dl, double (&r_in)[R][NA],
@@ -432,10 +521,12 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
 
   const int ngroups_in = (cols + K - 1) / K;
   const int ngroups = DP > 0 ? ngroups_in : (steps + K - 1) / K;
-  for (int c0 = 0, chunk = 0; c0 < steps; c0 += K, ++chunk) {
+  for (int c0 = c_begin * K, chunk = c_begin; c0 < steps && chunk < c_end; c0 += K, ++chunk) {
     __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
-    if (chunk + 1 < ngroups) {
-      if (has_below && !wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin)) return;
+    if (chunk + 1 < ngroups && chunk + 1 < c_end) {
+      if (streaming && has_below &&
+          !wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin))
+        return kBandAbort;
       stage_group(chunk + 1);
       cp_async_wait<1>();
     } else {
@@ -527,7 +618,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
       // columns handed up before / after this chunk
       const int done0 = min(max(jfirst, 0), cols);
       const int done1 = min(max(jfirst + kend, 0), cols);
-      if (done1 > done0 && (done1 == cols || done1 / kPublish != done0 / kPublish)) {
+      if (streaming && done1 > done0 && (done1 == cols || done1 / kPublish != done0 / kPublish)) {
         // bar.warp.sync orders every lane's column stores before lane 0's
         // release store (PTX memory model: barrier synchronisation is part
         // of causality order), so one release by one lane publishes them all
@@ -542,13 +633,25 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
       }
     }
   }
-  if (!has_above && P.bands > 1) {
+  if (streaming && !has_above && P.bands > 1) {
     // the last band publishes completion too: the slot's next pair (p + slots)
     // may only rewrite the column buffer once this band has read all of it
     cp_async_wait<0>();
     __syncwarp();
     if (lane == 0) st_release_gpu(prog_row + b, base + cols);
   }
+  if (save) {
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < NA; ++m)
+        if (NA <= kMaxRegOrder + 1 || m < n) rec[(r * NP + m) * 32 + lane] = roA[r][m];
+    for (int e = lane; e < 32 * R * NP; e += 32) rec[32 * R * NP + e] = s_pass[e];
+  }
+  // per-pair error key (first failing tile) and max|delta|: min / max
+  // reductions, so each segment flushes its part
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (jkey[r] != ~0u) atomicMin(P.err + out, err_key(irow[r], jkey[r] >> 2, jkey[r] & 3u));
@@ -560,6 +663,7 @@ __device__ __forceinline__ void sweep_band(const SweepParams& P, unsigned p, uns
         atomicMax(P.maxrho + out, static_cast<unsigned long long>(__double_as_longlong(mx)));
     }
   }
+  return kBandDone;
 }
 
 // Persistent: grid = resident CTAs; dynamic shared memory =
@@ -569,44 +673,134 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
   extern __shared__ __align__(16) double s_dyn[];
   double* smem = s_dyn + (threadIdx.x >> 5) * stage_doubles_per_warp(N, DP);
   const int lane = threadIdx.x & 31;
+  constexpr int H = 32 * rows_per_lane(N);
+  constexpr int K = chunk_cols(rows_per_lane(N));
   const unsigned nb = static_cast<unsigned>(P.band_end - P.band_begin);
-  const unsigned total_units = static_cast<unsigned>(P.npairs) * nb;
   const unsigned gsz = static_cast<unsigned>(P.group) * nb;
   for (;;) {
-    unsigned u = 0;
-    if (lane == 0) u = atomicAdd(P.queue, 1u);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= total_units) return;
-    if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) return;
-    // unit order: (group g, band b, pair q within the group)
-    const unsigned g = u / gsz;
-    const unsigned rem = u - g * gsz;
-    const unsigned g0 = g * static_cast<unsigned>(P.group);
-    const unsigned gcount = min(static_cast<unsigned>(P.group), static_cast<unsigned>(P.npairs) - g0);
-    const unsigned b = static_cast<unsigned>(P.band_begin) + rem / gcount;
-    const unsigned p = g0 + (rem - (b - static_cast<unsigned>(P.band_begin)) * gcount);
+    unsigned p, b;
+    int c_begin = 0, c_end = 0x7fffffff, seg = 0;
+    SegRange sr{0, 0};
+    bool restore = false, save = false;
+    if (P.seg_cols == 0) {
+      // streaming: static unit order (group g, band b, pair q within the group)
+      unsigned u = 0;
+      if (lane == 0) u = atomicAdd(P.queue, 1u);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= static_cast<unsigned>(P.npairs) * nb) return;
+      if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) return;
+      const unsigned g = u / gsz;
+      const unsigned rem = u - g * gsz;
+      const unsigned g0 = g * static_cast<unsigned>(P.group);
+      const unsigned gcount = min(static_cast<unsigned>(P.group), static_cast<unsigned>(P.npairs) - g0);
+      b = static_cast<unsigned>(P.band_begin) + rem / gcount;
+      p = g0 + (rem - (b - static_cast<unsigned>(P.band_begin)) * gcount);
+    } else {
+      // segment DAG: claim the next cell of the ready list, wait for its unit
+      unsigned u = 0;
+      if (lane == 0) {
+        const unsigned h = atomicAdd(P.ctr, 1u);
+        if (h >= P.units_total) {
+          u = ~0u;
+        } else {
+          const unsigned* cell = P.rq + h;
+          unsigned v, ns = 32;
+          const unsigned long long t0 = globaltimer_ns();
+          for (unsigned it = 1; (v = ld_acquire_u32(cell)) == 0u; ++it) {
+            __nanosleep(ns);
+            if (ns < 1024) ns *= 2;
+            if ((it & 63) == 0) {
+              if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) {
+                v = 0u;
+                break;
+              }
+              if (globaltimer_ns() - t0 > P.watchdog_ns) {
+                if (atomicCAS(P.watchdog, 0ull, 1ull) == 0ull) {
+                  P.watchdog[1] = ~0ull;
+                  P.watchdog[2] = ~0ull;
+                  P.watchdog[3] = h;
+                  P.watchdog[4] = ld_relaxed_u32(P.ctr + kCtrLine);
+                }
+                v = 0u;
+                break;
+              }
+            }
+          }
+          u = v - 1u;  // ~0u on abort
+        }
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u == ~0u) return;
+      __syncwarp();  // lane 0's acquire of the unit before every lane reads its inputs
+      const unsigned spb = static_cast<unsigned>(P.segs_per_band);
+      const unsigned pb = u / spb;
+      p = pb / static_cast<unsigned>(P.bands);
+      b = pb - p * static_cast<unsigned>(P.bands);
+      sr = seg_range(P.rows, P.cols, static_cast<int>(b), H, P.seg_cols);
+      seg = sr.lo + static_cast<int>(u - pb * spb);
+      // steps [seg L - b H, (seg+1) L - b H) clipped to the band: chunk range
+      c_begin = max(0, seg * P.seg_cols - static_cast<int>(b) * H) / K;
+      c_end = ((seg + 1) * P.seg_cols - static_cast<int>(b) * H) / K;
+      restore = seg > sr.lo;
+      save = seg < sr.hi;
+    }
 #ifdef SK_PROFILE_WAITS
     const long long t0 = clock64();
     const unsigned long long gt0 = globaltimer_ns();
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (lane == 0) g_wwait[wid] = 0;
-    sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem);
+    const int st = sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem, c_begin, c_end, restore, save);
     if (lane == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(P.watchdog + 7), clock64() - t0);
-      if (u < kTraceUnits) {
+      const unsigned t = atomicAdd(&g_tidx, 1u);
+      if (t < kTraceUnits) {
         unsigned smid, hwwarp;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         asm volatile("mov.u32 %0, %%warpid;" : "=r"(hwwarp));
         smid |= hwwarp << 8;
-        g_utrace[4 * u] = p | (static_cast<unsigned long long>(b) << 20) | (static_cast<unsigned long long>(smid) << 40);
-        g_utrace[4 * u + 1] = gt0;
-        g_utrace[4 * u + 2] = globaltimer_ns();
-        g_utrace[4 * u + 3] = g_wwait[wid];
+        g_utrace[4 * t] = p | (static_cast<unsigned long long>(b) << 20) | (static_cast<unsigned long long>(smid) << 40);
+        g_utrace[4 * t + 1] = gt0;
+        g_utrace[4 * t + 2] = globaltimer_ns();
+        g_utrace[4 * t + 3] = g_wwait[wid] | (static_cast<unsigned long long>(seg) << 40);
       }
     }
 #else
-    sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem);
+    const int st = sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem, c_begin, c_end, restore, save);
 #endif
+    if (st == kBandAbort) return;
+    if (P.seg_cols > 0) {
+      __syncwarp();  // every lane's outputs before lane 0 releases them
+      if (lane == 0) {
+        const unsigned spb = static_cast<unsigned>(P.segs_per_band);
+        const unsigned slot = p % static_cast<unsigned>(P.slots);
+        const size_t slot_base = static_cast<size_t>(slot) * P.bands * spb;
+        const unsigned unit_base = p * static_cast<unsigned>(P.bands) * spb;
+        // right neighbour (b, seg + 1): inputs (b, seg) and (b - 1, seg + 1)
+        if (seg < sr.hi) {
+          const SegRange below = b > 0 ? seg_range(P.rows, P.cols, static_cast<int>(b) - 1, H, P.seg_cols) : SegRange{0, -1};
+          const unsigned nd = 1u + (b > 0 && seg + 1 <= below.hi ? 1u : 0u);
+          const unsigned off = b * spb + static_cast<unsigned>(seg + 1 - sr.lo);
+          dep_arrive(P, slot_base + off, nd, unit_base + off);
+        }
+        // unit above (b + 1, seg): inputs (b + 1, seg - 1) and (b, seg)
+        if (b + 1 < static_cast<unsigned>(P.bands)) {
+          const SegRange above = seg_range(P.rows, P.cols, static_cast<int>(b) + 1, H, P.seg_cols);
+          if (seg >= above.lo) {
+            const unsigned nd = 1u + (seg > above.lo ? 1u : 0u);
+            const unsigned off = (b + 1) * spb + static_cast<unsigned>(seg - above.lo);
+            dep_arrive(P, slot_base + off, nd, unit_base + off);
+          }
+        }
+        // the pair's last unit: every other unit of the pair is done (all are
+        // its ancestors) -- recycle the slot's counters, queue the next pair
+        const bool last = b + 1 == static_cast<unsigned>(P.bands) && seg == sr.hi;
+        if (last && p + P.slots < static_cast<unsigned>(P.npairs)) {
+          for (size_t k = 0; k < static_cast<size_t>(P.bands) * spb; ++k) P.dep[slot_base + k] = 0u;
+          rq_push(P, (p + P.slots) * static_cast<unsigned>(P.bands) * spb);
+        }
+        atomicAdd(P.ctr + 2 * kCtrLine, 1u);
+      }
+    }
   }
 }
 

@@ -48,6 +48,15 @@ template <int N, int DP, bool EXACT, bool EXTRAS>
 static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& P) {
   cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
   if (e != cudaSuccess) return e;
+#ifdef SK_PROFILE_WAITS
+  {
+    static const unsigned zero = 0;
+    cudaMemcpyToSymbolAsync(g_tidx, &zero, sizeof zero, 0, cudaMemcpyHostToDevice, stream);
+    void* tp = nullptr;
+    cudaGetSymbolAddress(&tp, g_utrace);
+    cudaMemsetAsync(tp, 0, kTraceUnits * 4 * sizeof(unsigned long long), stream);
+  }
+#endif
   sweep_kernel<N, DP, EXACT, EXTRAS><<<grid, kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>(), stream>>>(P);
 #ifdef SK_PROFILE_WAITS
   if (const char* path = std::getenv("SK_UTRACE")) {

@@ -236,6 +236,64 @@ def test_slot_reuse_and_groups_are_deterministic(sk, restatement, monkeypatch):
         assert rel(base[k], restatement.propagate(xs[k], ys[k], 8)[0]) < TOL
 
 
+@pytest.mark.parametrize("seg_cols", ["32", "96"])
+def test_segment_dag_matches_streaming(sk, restatement, monkeypatch, seg_cols):
+    """The segment-DAG schedule (units = band segments, dependency counters,
+    lane state carried between segments) computes exactly what the streaming
+    schedule computes: values, orders, max|rho|, errors, knot grids -- across
+    register / literal / table kernels, ragged shapes and slot reuse."""
+    rng = restatement.rng(2024)
+    cases = []
+    for (lx, ly, d, order) in [(70, 100, 3, 8), (130, 97, 2, 12), (66, 200, 8, 20), (90, 64, 40, 8), (41, 150, 16, 5)]:
+        xs = np.stack([rng.random_series(lx, d, 1.0) for _ in range(5)])
+        ys = np.stack([rng.random_series(ly, d, 1.0) for _ in range(5)])
+        cases.append((xs, ys, order))
+
+    # a pair that overflows inside the sweep
+    x = rng.random_series(80, 1, 1.0)
+    y = rng.random_series(90, 1, 1.0)
+    x[40:] *= 3e4
+    y[50:] *= 3e4
+
+    def bits(v):
+        return np.ascontiguousarray(v, dtype=np.float64).view(np.int64).tolist()
+
+    def run_all():
+        out = []
+        for xs, ys, order in cases:
+            r = sk.pairwise(xs, ys, sk.TruncationPolicy.fixed(order))
+            out.append(bits(r.values))
+            a = sk.pairwise(xs, ys, sk.TruncationPolicy.adaptive(1e-12), want_max_abs_rho=True)
+            out.append((bits(a.values), list(a.orders), bits(a.max_abs_rho)))
+            g = sk.propagate_grid(xs[0], ys[0], order)
+            out.append(bits(g.grid))
+        # an overflow inside the sweep: first failing tile, as streaming reports it
+        for strict in (True, False):
+            try:
+                out.append(bits([sk.propagate(x, y, 8, sk.PropagateOptions(strict_corner=strict)).value]))
+            except sk.NumericOverflowError as e:
+                out.append(("overflow", e.tile_k, e.tile_l))
+            except sk.InconsistentBoundaryError as e:
+                out.append(("corner", str(e)))
+        return out
+
+    monkeypatch.setenv("SK_STREAM", "1")
+    ref = run_all()
+    monkeypatch.delenv("SK_STREAM")
+    monkeypatch.setenv("SK_FORCE_SEGMENTS", "1")
+    monkeypatch.setenv("SK_SEG_COLS", seg_cols)
+
+    def check(got):
+        assert len(got) == len(ref)
+        for k, (a, b) in enumerate(zip(got, ref)):
+            assert a == b, (k, str(a)[:300], str(b)[:300])
+
+    check(run_all())
+    monkeypatch.setenv("SK_FORCE_SLOTS", "2")
+    monkeypatch.setenv("SK_FORCE_GROUP", "1")
+    check(run_all())
+
+
 def test_thread_safety_and_determinism(sk, restatement):
     rng = restatement.rng(123)
     pairs = [(rng.random_series(60, 2, 1.0), rng.random_series(45, 2, 1.0)) for _ in range(8)]
