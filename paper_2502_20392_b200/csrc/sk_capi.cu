@@ -367,15 +367,32 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // units per launch must fit 32 bits
   chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / bands));
 
-  // Segment-DAG geometry (SweepParams::seg_cols): used when the launch sweeps
-  // whole pairs with several units per warp; streaming otherwise (a
-  // latency-bound single short pair, multi-GPU strips).
+  // Segment-DAG geometry (SweepParams::seg_cols).  The DAG of a pair is a
+  // bands x segments grid worked in anti-diagonal waves: it needs enough units
+  // per wave to fill the warps (pairs in flight x min(bands, segments)) and a
+  // critical path ((bands + segments) x L steps) well below the per-warp
+  // work.  The largest segment length L in {256, 128, 64} that meets both is
+  // used; otherwise the streaming schedule (a latency-bound short pair, a
+  // single long pair with few columns per band, multi-GPU strips).
   const bool whole = strip.band_begin == 0 && strip.band_end < 0 && strip.xin_band < 0 && strip.xout_band < 0;
   int seg_cols = 0;
   unsigned spb = 0, units_pair = 0;
   if (bands > 1 && whole && std::getenv("SK_STREAM") == nullptr) {
-    seg_cols = 256;  // B200, N = 8: 256 x 4096^2 62.1 % of the FP64 roof (128: 62.1, 512: 59.1, streaming 57.1)
+    const double warps_est = static_cast<double>(bps) * c.sms * kSweepWarps;
+    const double pairs_launch = static_cast<double>(std::min(chunk, npairs_all));
+    const double active = std::min(pairs_launch, 2.0 * warps_est);
+    const double work_steps = pairs_launch * bands * (cols + 31.0) / warps_est;
+    const bool force = std::getenv("SK_FORCE_SEGMENTS") != nullptr;
+    for (int L : {256, 128, 64}) {
+      const double S = std::ceil((cols + 31.0) / L);
+      if (force || (active * std::min<double>(bands, S) >= 2.0 * warps_est && (bands + S) * L <= 0.5 * work_steps)) {
+        seg_cols = L;
+        break;
+      }
+    }
     if (const char* e = std::getenv("SK_SEG_COLS")) seg_cols = std::atoi(e);
+  }
+  if (seg_cols > 0) {
     seg_cols = std::max(band_rows, (seg_cols + band_rows - 1) / band_rows * band_rows);  // multiple of K and H
     for (int b = 0; b < bands; ++b) {
       const SegRange r = seg_range(rows, cols, b, band_rows, seg_cols);
@@ -426,8 +443,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     SK_CUDA(c.wd.ensure(8 * sizeof(unsigned long long)));
     SK_CUDA(cudaMemsetAsync(c.wd.p, 0, 8 * sizeof(unsigned long long), c.stream()));
     if (bands > 1) SK_CUDA(c.abuf.ensure(slots * col_bytes));
-    // segment mode only with several units per warp (SK_FORCE_SEGMENTS: always, for tests)
-    const int seg_here = (units >= 4ull * warps || std::getenv("SK_FORCE_SEGMENTS") != nullptr) ? seg_cols : 0;
+    const int seg_here = seg_cols;
     if (seg_here > 0) {
       const size_t nrec = slots * static_cast<size_t>(bands);
       SK_CUDA(c.susp.ensure(nrec * static_cast<size_t>(susp_record_doubles(ntempl)) * sizeof(double)));
