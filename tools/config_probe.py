@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--len3", type=int, default=1_000_001)
     ap.add_argument("--sigma3", type=float, default=1.0)
     ap.add_argument("--m5", type=int, default=128)
+    ap.add_argument("--warm", action="store_true", help="cfg5: one small Gram first (kernel loading, allocations)")
     a = ap.parse_args()
     pol = sk.TruncationPolicy.adaptive(1e-12)
     for cfg in a.configs:
@@ -74,6 +75,8 @@ def main():
         elif cfg == "cfg5":
             m = a.m5
             fam = list(brownian(m, 4096, 16, 1000))
+            if a.warm:
+                sk.gram_matrix(fam[:8], sk.GramOptions(policy=pol))
             r, wall, s = timed(lambda: sk.gram_matrix(fam, sk.GramOptions(policy=pol)))
             npairs = m * (m + 1) // 2
             report(f"cfg5 Gram m={m} l=4096 d=16", npairs * 4095 ** 2, wall, s,
