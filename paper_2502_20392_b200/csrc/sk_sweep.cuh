@@ -49,11 +49,14 @@ constexpr int kSweepWarps = SK_SWEEP_WARPS;
 // SM sub-partition holds 16K registers, so <= 168 registers/thread gives 3
 // warps per sub-partition (12 per SM), more gives only 2.  Orders up to 10
 // fit 168 without spills; larger orders keep the unconstrained allocation.
+#ifndef SK_ROWS_PER_LANE
+#define SK_ROWS_PER_LANE 1
+#endif
 #ifndef SK_MIN_BLOCKS
 #define SK_MIN_BLOCKS 0
 #endif
 __host__ __device__ constexpr int sweep_min_blocks(int N) {
-  return SK_MIN_BLOCKS > 0 ? SK_MIN_BLOCKS : (N >= 1 && N <= 10 ? 12 : 1);
+  return SK_MIN_BLOCKS > 0 ? SK_MIN_BLOCKS : (N >= 1 && N <= 10 ? (SK_ROWS_PER_LANE == 2 ? 8 : 12) : 1);
 }
 
 // Rows per lane.  R = 2: a warp sweeps a 64-row band, lane t owning rows t
@@ -62,9 +65,6 @@ __host__ __device__ constexpr int sweep_min_blocks(int N) {
 // (N = 8, d = 8, 256 x 4096^2): R = 1 68 ms, R = 2 77 ms (200 registers, 8
 // warps/SM, smaller chunks) -- R = 1 is the default; the literal kernel
 // (N = 0, series in local memory) always uses R = 1.
-#ifndef SK_ROWS_PER_LANE
-#define SK_ROWS_PER_LANE 1
-#endif
 __host__ __device__ constexpr int rows_per_lane(int N) { return N > 0 ? SK_ROWS_PER_LANE : 1; }
 // columns per staging group / delta batch
 __host__ __device__ constexpr int chunk_cols(int R) { return R == 2 ? 8 : 16; }
