@@ -371,9 +371,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // bands x segments grid worked in anti-diagonal waves: it needs enough units
   // per wave to fill the warps (pairs in flight x min(bands, segments)) and a
   // critical path ((bands + segments) x L steps) well below the per-warp
-  // work.  The largest segment length L in {256, 128, 64} that meets both is
-  // used; otherwise the streaming schedule (a latency-bound short pair, a
-  // single long pair with few columns per band, multi-GPU strips).
+  // work.  The largest segment length L in {256, 128, 64} that meets both
+  // (critical path under half the work, else under the work) is used;
+  // otherwise the streaming schedule (a latency-bound short pair, multi-GPU
+  // strips).
   const bool whole = strip.band_begin == 0 && strip.band_end < 0 && strip.xin_band < 0 && strip.xout_band < 0;
   int seg_cols = 0;
   unsigned spb = 0, units_pair = 0;
@@ -383,12 +384,18 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     const double active = std::min(pairs_launch, 2.0 * warps_est);
     const double work_steps = pairs_launch * bands * (cols + 31.0) / warps_est;
     const bool force = std::getenv("SK_FORCE_SEGMENTS") != nullptr;
-    for (int L : {256, 128, 64}) {
-      const double S = std::ceil((cols + 31.0) / L);
-      if (force || (active * std::min<double>(bands, S) >= 2.0 * warps_est && (bands + S) * L <= 0.5 * work_steps)) {
-        seg_cols = L;
-        break;
+    // measured (N = 8): 256 pairs x 4096^2 best at L = 256/128; one pair of
+    // 262144^2 best at 64 (57 % vs 47 % streaming), of 10^6 at 128
+    for (const double crit_frac : {0.5, 1.0}) {
+      for (int L : {256, 128, 64}) {
+        const double S = std::ceil((cols + 31.0) / L);
+        if (force ||
+            (active * std::min<double>(bands, S) >= 2.0 * warps_est && (bands + S) * L <= crit_frac * work_steps)) {
+          seg_cols = L;
+          break;
+        }
       }
+      if (seg_cols) break;
     }
     if (const char* e = std::getenv("SK_SEG_COLS")) seg_cols = std::atoi(e);
   }
