@@ -100,7 +100,7 @@ __host__ __device__ constexpr double kFactRatio(int m) {
 // the sign of the W[1][1] contribution (the reference's negative-control
 // hook, tile_series.cpp:51-52).
 template <int N>
-__device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
+__device__ __forceinline__ void tile_update_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
                                                    double (&qo)[N + 1], double (&ro)[N + 1], bool fault) {
   constexpr int n = N + 1;
   // ph[m] = delta^m / N! by a depth-4 product tree (d2 = delta^2, d4 = delta^4);
@@ -166,8 +166,12 @@ __device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], con
       ro[1] -= c11;
     }
   }
-  // total = sum_a q'[a] / a! = (1/N!) sum_a q'[a] (N!/a!): two interleaved
-  // accumulators with integer immediate weights (short dependency chains)
+}
+
+// total = sum_a q'[a] / a! = (1/N!) sum_a q'[a] (N!/a!): two interleaved
+// accumulators with integer immediate weights (short dependency chains)
+template <int N>
+__device__ __forceinline__ double scaled_total(const double (&qo)[N + 1]) {
   double te = qo[N], to = 0.0;
 #pragma unroll
   for (int a = N - 1; a >= 0; --a) {
@@ -179,6 +183,15 @@ __device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], con
   const double tot = te + to;
   return tot * c_inv_fact[N];
 }
+
+// One tile on factorial-scaled series; returns the total.
+template <int N>
+__device__ __forceinline__ double tile_step_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
+                                                   double (&qo)[N + 1], double (&ro)[N + 1], bool fault) {
+  tile_update_scaled<N>(q, r, delta, qo, ro, fault);
+  return scaled_total<N>(qo);
+}
+
 
 // Literal reference tile step (wavefront.cpp:35-59) on UNSCALED series with a
 // runtime order: same expression `b * (pw[min(i,j)] * w[i][j])`, row sums over

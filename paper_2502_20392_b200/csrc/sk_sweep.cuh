@@ -488,9 +488,13 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       const int j = s - lane - 32 * r;
       const double delta = dl[(r * K + k) * 32 + lane];
       double qo[NA];
-      double total;
+      double total = 0.0;
       if constexpr (N > 0) {
-        total = tile_step_scaled<N>(q[r], r_in[r], delta, qo, ro_out[r], fault);
+        // the total is formed at every tile: the error contract needs it
+        // (non-finite total, wavefront.cpp:169-173).  Measured: skipping it
+        // behind an integer finiteness screen costs more than it saves.
+        tile_update_scaled<N>(q[r], r_in[r], delta, qo, ro_out[r], fault);
+        total = scaled_total<N>(qo);
       } else {
         total = tile_step_literal(P.order, q[r], r_in[r], delta, P.w65, qo, ro_out[r]);
       }
