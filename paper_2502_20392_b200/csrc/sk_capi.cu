@@ -356,6 +356,24 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   }
   const size_t free_b = c.free_cache;
   tr.mark("  occupancy+memgetinfo");
+  // EXACT register kernels form the fast (fused) dot per tile and the
+  // sequential one only where it could raise the exact max: they need a bound
+  // on |fused - sequential| <= 2 d u sum|x_c y_c| <= 2 d u max||dx|| max||dy||
+  double dot_err = 0.0;
+  if (exact && ntempl > 0 && dp > 0) {
+    const uint32_t nx = 1 + *std::max_element(px.begin(), px.end());
+    const uint32_t ny = 1 + *std::max_element(py.begin(), py.end());
+    SK_CUDA(c.sqn.ensure((nx + ny) * sizeof(double)));
+    SK_CUDA(launch_max_sqnorm(ps.d_xinc, nx, cols, ps.dim, ps.ld, c.sqn.as<double>(), c.stream()));
+    SK_CUDA(launch_max_sqnorm(ps.d_yinc, ny, rows, ps.dim, ps.ld, c.sqn.as<double>() + nx, c.stream()));
+    c.aux_launches += 2;
+    std::vector<double> h(nx + ny);
+    SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, (nx + ny) * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    SK_CUDA(cudaStreamSynchronize(c.stream()));
+    const double mxx = *std::max_element(h.begin(), h.begin() + nx);
+    const double mxy = *std::max_element(h.begin() + nx, h.end());
+    dot_err = 4.0 * ps.dim * std::ldexp(1.0, -53) * std::sqrt(mxx * mxy) * 1.01 + 1e-300;
+  }
 
   // large d: per-pair rho tables (rows x cols), pairs chunked to a memory budget
   const size_t tab_elems = dp == 0 ? static_cast<size_t>(rows) * cols : 0;
@@ -510,6 +528,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     // with fewer pairs than warps, ~warps/group bands of each pair run at
     // once; their natural spacing is one band time / (warps / group)
     P.start_lag = group < warps ? static_cast<int>(0.75 * (cols + 32.0) * group / warps) : 0;
+    P.dot_err = dot_err;
     if (const char* e = std::getenv("SK_START_LAG")) P.start_lag = std::atoi(e);
     P.values = o.d_values;
     P.err = o.d_err;

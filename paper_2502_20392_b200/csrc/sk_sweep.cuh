@@ -90,6 +90,7 @@ struct SweepParams {
   unsigned long long* watchdog;   // [0] abort flag, [1..4] first stuck wait (p, b, need, seen)
   unsigned long long watchdog_ns; // give up a dependency wait after this long
   int start_lag;                  // columns the band below must be ahead before a band starts
+  double dot_err;                 // EXACT, N > 0: bound on |fused dot - sequential dot| for any tile
   double* values;                 // per output slot: K(1,1)
   unsigned long long* err;        // per output slot: min error key (init ~0)
   unsigned long long* maxrho;     // per output slot: max |delta| bits (init 0) or null
@@ -367,7 +368,12 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int m = 0; m < NA; ++m) roA[r][m] = (m == 0) ? 1.0 : 0.0;
+  // running exact max|delta| of this band: start from the pair's value so far
+  // (a valid lower bound) so fewer tiles need the exact dot
   double mx = 0.0;
+  if constexpr (EXACT && N > 0) {
+    if (P.maxrho) mx = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.maxrho + out)));
+  }
   unsigned jkey[R];  // (first failing column << 2) | code, per tile
 #pragma unroll
   for (int r = 0; r < R; ++r) jkey[r] = ~0u;
@@ -563,8 +569,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if constexpr (EXACT) {
-              dd[u] = exact_dot<DP>(dx[u], dy);
+            if constexpr (EXACT && N == 0) {
+              dd[u] = exact_dot<DP>(dx[u], dy);  // the literal kernel repeats the reference bit for bit
             } else {
               double e0 = dx[u][0] * dy[0], e1 = dx[u][1] * dy[1];
 #pragma unroll
@@ -580,15 +586,35 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
 #pragma unroll
           for (int u = 0; u < 4; ++u) dd[u] = dl[(r * K + k0 + u) * 32 + lane];
         }
+        unsigned cand = 0u;  // EXACT, N > 0: tiles whose exact |delta| could raise the running max
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int k = k0 + u;
           const int j = c0 + k - lane - 32 * r;
           const bool act = row_ok[r] && j >= 0 && j < cols && k < kend;
           const double ad = fabs(dd[u]);
-          if constexpr (EXACT) mx = fmax(mx, act ? ad : 0.0);
+          if constexpr (EXACT && (N == 0 || DP == 0)) mx = fmax(mx, act ? ad : 0.0);  // dd is exact here
+          if constexpr (EXACT && N > 0 && DP > 0) cand |= (act && ad + P.dot_err >= mx) ? 1u << u : 0u;
           const unsigned kk = (static_cast<unsigned>(j) << 2) | kErrDelta;
           jkey[r] = min(jkey[r], (act && !(ad <= kDeltaOverflowLimit)) ? kk : ~0u);
+        }
+        if constexpr (EXACT && N > 0 && DP > 0) {
+          // exact max|delta| (bit-identical to max_abs_rho) without an exact
+          // dot per tile: |fused - sequential| <= dot_err, so only a tile whose
+          // fused |delta| + dot_err reaches the running exact max can raise it
+          // -- rare once the max has settled; those get the sequential dot,
+          // re-reading their dx row from the ring
+          if (__any_sync(0xffffffffu, cand != 0u)) {
+#pragma unroll 1
+            for (int u = 0; u < 4; ++u)
+              if ((cand >> u) & 1u) {
+                const double* xr = s_ring + ((c0 + k0 + u - lane - 32 * r) & (RING - 1)) * XS;
+                double row[DP];
+#pragma unroll
+                for (int c = 0; c < DP; ++c) row[c] = xr[c];
+                mx = fmax(mx, fabs(exact_dot<DP>(row, dy)));
+              }
+          }
         }
       }
     }
