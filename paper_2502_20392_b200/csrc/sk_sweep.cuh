@@ -303,6 +303,13 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   constexpr int NP = col_stride(N);
   constexpr int XS = ring_stride(DP);
   constexpr int kStage = K * NP;
+#ifndef SK_INLINE_DELTA
+#define SK_INLINE_DELTA 1
+#endif
+  // increments products formed inside the step (not per chunk) where the
+  // registers allow it: d <= 8, register kernels, no exact max.  Measured:
+  // 256 x 4096^2 62.95 vs 63.5 ms; at d = 16 it spills and gains nothing.
+  constexpr bool kInlineDelta = SK_INLINE_DELTA && DP > 0 && DP <= 8 && N > 0 && !EXACT && R == 1;
   double* s_alpha = smem;                                   // 2 x K x NP
   double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
   double* s_out = s_pass + 32 * R * NP;                     // K x NP
@@ -492,7 +499,26 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int j = s - lane - 32 * r;
-      const double delta = dl[(r * K + k) * 32 + lane];
+      double delta;
+      if constexpr (kInlineDelta) {
+        // this tile's increment product, formed in the step (its loads and
+        // FMAs overlap the tile math's dependency chains) with its guard
+        const double* xr = s_ring + ((s - lane - 32 * r) & (RING - 1)) * XS;
+        double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < DP; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(xr + c);
+          e0 = fma(v.x, dyr[r][c], e0);
+          e1 = fma(v.y, dyr[r][c + 1], e1);
+        }
+        delta = e0 + e1;
+        const bool act = row_ok[r] && j >= 0 && j < cols;
+        jkey[r] = min(jkey[r], (act && !(fabs(delta) <= kDeltaOverflowLimit))
+                                   ? (static_cast<unsigned>(j) << 2) | kErrDelta
+                                   : ~0u);
+      } else {
+        delta = dl[(r * K + k) * 32 + lane];
+      }
       double qo[NA];
       double total = 0.0;
       if constexpr (N > 0) {
@@ -549,7 +575,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     // the chunk's increment products (tile r, step c0 + k -> column
     // c0 + k - t - 32 r) with the delta guard (wavefront.cpp:150-155) and max|delta|
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < (kInlineDelta ? 0 : R); ++r) {
       const double (&dy)[DP > 0 ? DP : 1] = dyr[r];
 #pragma unroll 1
       for (int k0 = 0; k0 < K; k0 += 4) {
