@@ -89,7 +89,11 @@ class TimeSeries:
             raise ValueError("time series must contain at least one point")
         if v.size % dim != 0:
             raise ValueError("value count is not a multiple of the dimension")
-        if not np.all(np.isfinite(v)):
+        # time_series.cpp:9-19.  A finite sum proves every value finite (NaN and
+        # inf propagate); only an overflowing sum needs the elementwise test
+        with np.errstate(over="ignore", invalid="ignore"):
+            total = float(v.sum())
+        if not (math.isfinite(total) or np.all(np.isfinite(v))):
             raise ValueError("time series coordinates must be finite")
         self._v = v.reshape(-1, dim)
         self._v.setflags(write=False)
