@@ -3,6 +3,7 @@
 // Status codes come back as the reference's exception types.
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -176,10 +177,62 @@ GramResult gram_matrix(const std::vector<TimeSeries>& family, const GramOptions&
   const uint32_t flags = (options.strict_corner ? SK_STRICT_CORNER : 0u) |
                          (tile::detail::w_fault_for_testing() ? SK_W_FAULT : 0u);
   const auto t0 = std::chrono::steady_clock::now();
-  check(sk_gram(buf.data(), m, max_len, dim, adaptive ? 1 : 0, options.policy.order, options.policy.tol, flags,
-                scan ? 1 : 0, options.shard, options.nshards, r.values.data(), r.orders.data(), nullptr, &maxp, &conv,
-                per.data(), &st),
-        st);
+  const std::size_t nd = options.devices.size();
+  if (nd <= 1) {
+    if (nd == 1) check(sk_set_device(options.devices[0], &st), st);
+    check(sk_gram(buf.data(), m, max_len, dim, adaptive ? 1 : 0, options.policy.order, options.policy.tol, flags,
+                  scan ? 1 : 0, options.shard, options.nshards, r.values.data(), r.orders.data(), nullptr, &maxp,
+                  &conv, per.data(), &st),
+          st);
+  } else {
+    // one host thread per device, each a sub-shard (shard * nd + k of nshards * nd);
+    // every thread owns its context, so the calls run concurrently
+    struct Part {
+      std::vector<double> values;
+      std::vector<int> orders;
+      std::vector<sk_status> per;
+      double maxp = 0.0;
+      int conv = 1;
+      sk_status st{};
+      int rc = SK_OK;
+    };
+    std::vector<Part> parts(nd);
+    std::vector<std::thread> pool;
+    for (std::size_t k = 0; k < nd; ++k)
+      pool.emplace_back([&, k] {
+        Part& pt = parts[k];
+        pt.values.assign(m * m, 0.0);
+        pt.orders.assign(m * m, 0);
+        pt.per.assign(m * m, sk_status{});
+        pt.rc = sk_set_device(options.devices[k], &pt.st);
+        if (pt.rc == SK_OK)
+          pt.rc = sk_gram(buf.data(), m, max_len, dim, adaptive ? 1 : 0, options.policy.order, options.policy.tol,
+                          flags, scan ? 1 : 0, options.shard * nd + k, options.nshards * nd, pt.values.data(),
+                          pt.orders.data(), nullptr, &pt.maxp, &pt.conv, pt.per.data(), &pt.st);
+      });
+    for (auto& t : pool) t.join();
+    for (Part& pt : parts) check(pt.rc, pt.st);
+    // entry t of the upper triangle (row-major) belongs to the sub-shard whose range holds it
+    std::size_t t = 0;
+    std::vector<std::pair<std::size_t, std::size_t>> ranges(nd);
+    for (std::size_t k = 0; k < nd; ++k)
+      sk_gram_shard_range(m, options.shard * nd + k, options.nshards * nd, &ranges[k].first, &ranges[k].second);
+    for (std::size_t i = 0; i < m; ++i)
+      for (std::size_t j = i; j < m; ++j, ++t)
+        for (std::size_t k = 0; k < nd; ++k)
+          if (t >= ranges[k].first && t < ranges[k].second) {
+            for (const std::size_t e : {i * m + j, j * m + i}) {
+              r.values[e] = parts[k].values[e];
+              r.orders[e] = parts[k].orders[e];
+              per[e] = parts[k].per[e];
+            }
+            break;
+          }
+    for (const Part& pt : parts) {
+      maxp = std::max(maxp, pt.maxp);
+      conv = conv && pt.conv;
+    }
+  }
   r.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   r.orders_converged = conv != 0;
   for (std::size_t i = 0; i < m; ++i)

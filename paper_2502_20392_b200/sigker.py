@@ -454,6 +454,9 @@ class GramOptions:
     threads: int = 1
     compute_bound: bool = False
     strict_corner: bool = True
+    # GPUs to spread this call over, one host thread each (a sub-shard per
+    # device); empty: the current device
+    devices: List[int] = field(default_factory=list)
 
 
 @dataclass
@@ -526,11 +529,59 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     if _W_FAULT[0]:
         flags |= _capi.SK_W_FAULT
     t0 = time.perf_counter()
-    rc = lib.sk_gram(_ptr(padded), m, max_len, dim, 1 if adaptive else 0, int(options.policy.order),
-                     float(options.policy.tol), flags, 1 if scan else 0, int(shard), int(nshards), _ptr(values),
-                     _ptr(orders), _ptr(pmax), ctypes.byref(maxp), ctypes.byref(conv), per, ctypes.byref(st))
+
+    def run_shard(sub, nsub, vals, ords, pm, mp, cv, pr, status):
+        return lib.sk_gram(_ptr(padded), m, max_len, dim, 1 if adaptive else 0, int(options.policy.order),
+                           float(options.policy.tol), flags, 1 if scan else 0, int(sub), int(nsub), _ptr(vals),
+                           _ptr(ords), _ptr(pm), ctypes.byref(mp), ctypes.byref(cv), pr, ctypes.byref(status))
+
+    devices = list(options.devices)
+    if len(devices) <= 1:
+        if devices:
+            _check(lib.sk_set_device(int(devices[0]), ctypes.byref(st)), st)
+        rc = run_shard(shard, nshards, values, orders, pmax, maxp, conv, per, st)
+        _check(rc, st)
+    else:
+        # one host thread per GPU (ctypes releases the GIL during the call);
+        # each evaluates the sub-shard shard * nd + k of nshards * nd
+        import threading
+        nd = len(devices)
+        parts = [dict(values=np.zeros(m * m), orders=np.zeros(m * m, dtype=np.int32), pmax=np.zeros(m * m),
+                      maxp=ctypes.c_double(), conv=ctypes.c_int(), per=(_capi.SkStatus * (m * m))(),
+                      st=_capi.SkStatus(), rc=0) for _ in range(nd)]
+
+        def work(k):
+            p = parts[k]
+            p["rc"] = lib.sk_set_device(int(devices[k]), ctypes.byref(p["st"]))
+            if p["rc"] == 0:
+                p["rc"] = run_shard(shard * nd + k, nshards * nd, p["values"], p["orders"], p["pmax"], p["maxp"],
+                                    p["conv"], p["per"], p["st"])
+
+        threads = [threading.Thread(target=work, args=(k,)) for k in range(nd)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for p in parts:
+            _check(p["rc"], p["st"])
+        lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
+        owner = np.full(m * m, -1)
+        tri = [(i, j) for i in range(m) for j in range(i, m)]
+        for k in range(nd):
+            lib.sk_gram_shard_range(m, shard * nd + k, nshards * nd, ctypes.byref(lo), ctypes.byref(hi))
+            for (i, j) in tri[lo.value:hi.value]:
+                owner[i * m + j] = owner[j * m + i] = k
+        values[:] = np.nan
+        for k, p in enumerate(parts):
+            sel = owner == k
+            values[sel] = p["values"][sel]
+            orders[sel] = p["orders"][sel]
+            pmax[sel] = p["pmax"][sel]
+            for e in np.nonzero(sel)[0]:
+                per[e] = p["per"][e]
+        maxp.value = max(p["maxp"].value for p in parts)
+        conv.value = int(all(p["conv"].value for p in parts))
     wall = time.perf_counter() - t0
-    _check(rc, st)
     r = GramResult(size=m, values=values, orders=orders, adaptive=adaptive, orders_converged=bool(conv.value),
                    wall_seconds=wall)
     for i in range(m):

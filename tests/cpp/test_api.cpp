@@ -172,6 +172,13 @@ int main() {
   }
   for (std::size_t i = 0; i < 5; ++i)
     for (std::size_t j = i; j < 5; ++j) CHECK(close(gm.values[i * 5 + j], propagate(fam[i], fam[j], 20).value, 1e-10));
+  {
+    // GramOptions::devices: one host thread per listed GPU (here GPU 0 twice), merged bit for bit
+    GramOptions two{TruncationPolicy::fixed(20)};
+    two.devices = {0, 0};
+    const auto g2 = gram_matrix(fam, two);
+    CHECK(g2.values == gm.values && g2.orders == gm.orders);
+  }
   const auto fail = gram_matrix({s1({0.0, 1.0}), s1({0.0, 1e4})}, {TruncationPolicy::fixed(8)});
   CHECK(!fail.failures.empty() && fail.failures.front().row == 1 && fail.failures.front().col == 1);
   CHECK(std::isnan(fail.values[3]) && std::isfinite(fail.values[0]) && std::isfinite(fail.values[1]));

@@ -416,3 +416,18 @@ def test_strip_protocol_emulated_on_one_gpu(sk, restatement):
         assert nb >= 3
         for split in range(1, nb):
             assert propagate_split_emulated(x, y, order, split) == plain, (order, split)
+
+
+def test_gram_over_a_device_list_matches_one_call(sk, restatement):
+    """GramOptions.devices: one host thread per listed GPU, each a sub-shard
+    (here the same GPU twice -- independent pairs, no cross-kernel waits);
+    the merged matrix equals the single-call one bit for bit."""
+    rng = restatement.rng(404)
+    fam = [rng.random_series(40 + 3 * k, 2, 1.0) for k in range(9)]
+    pol = sk.TruncationPolicy.adaptive(1e-12)
+    one = sk.gram_matrix(fam, sk.GramOptions(policy=pol, compute_bound=True))
+    two = sk.gram_matrix(fam, sk.GramOptions(policy=pol, compute_bound=True, devices=[0, 0]))
+    assert np.asarray(two.values).view(np.int64).tolist() == np.asarray(one.values).view(np.int64).tolist()
+    assert list(two.orders) == list(one.orders)
+    assert two.max_abs_increment_product == one.max_abs_increment_product
+    assert two.orders_converged == one.orders_converged
