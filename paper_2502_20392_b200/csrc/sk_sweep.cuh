@@ -846,12 +846,16 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
           const unsigned off = b * spb + static_cast<unsigned>(seg + 1 - sr.lo);
           dep_arrive(P, slot_base + off, nd, unit_base + off);
         }
-        // unit above (b + 1, seg): inputs (b + 1, seg - 1) and (b, seg)
+        // the unit above that this one completes: (b + 1, seg), or -- from the
+        // band's last segment, when band b + 1 starts later (one-column pairs)
+        // -- band b + 1's first segment; inputs: its left neighbour (if any)
+        // and this unit
         if (b + 1 < static_cast<unsigned>(P.bands)) {
           const SegRange above = seg_range(P.rows, P.cols, static_cast<int>(b) + 1, H, P.seg_cols);
-          if (seg >= above.lo) {
-            const unsigned nd = 1u + (seg > above.lo ? 1u : 0u);
-            const unsigned off = (b + 1) * spb + static_cast<unsigned>(seg - above.lo);
+          const int tgt = seg == sr.hi ? max(seg, above.lo) : seg;
+          if (tgt >= above.lo) {
+            const unsigned nd = 1u + (tgt > above.lo ? 1u : 0u);
+            const unsigned off = (b + 1) * spb + static_cast<unsigned>(tgt - above.lo);
             dep_arrive(P, slot_base + off, nd, unit_base + off);
           }
         }

@@ -244,7 +244,8 @@ def test_segment_dag_matches_streaming(sk, restatement, monkeypatch, seg_cols):
     register / literal / table kernels, ragged shapes and slot reuse."""
     rng = restatement.rng(2024)
     cases = []
-    for (lx, ly, d, order) in [(70, 100, 3, 8), (130, 97, 2, 12), (66, 200, 8, 20), (90, 64, 40, 8), (41, 150, 16, 5)]:
+    for (lx, ly, d, order) in [(70, 100, 3, 8), (130, 97, 2, 12), (66, 200, 8, 20), (90, 64, 40, 8), (41, 150, 16, 5),
+                               (2, 300, 2, 8), (3, 170, 1, 6)]:
         xs = np.stack([rng.random_series(lx, d, 1.0) for _ in range(5)])
         ys = np.stack([rng.random_series(ly, d, 1.0) for _ in range(5)])
         cases.append((xs, ys, order))

@@ -216,3 +216,19 @@ def test_strip_partition_and_error_order():
     recs = [(2, 10, 40, "a"), (2, 20, 30, "c")]  # same diagonal: lower row first
     assert first_error(recs)[3] == "c"
     assert first_error([None, None]) is None
+
+
+def test_segment_dag_model():
+    """The segment-DAG schedule's dependency rules (tools/segment_dag_sim.py
+    mirrors csrc/sk_sweep.cuh): every unit runs once, after its inputs, for
+    ragged shapes including one-column pairs (the band above starts later than
+    the band below ends) and slot reuse."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("segsim", os.path.join(ROOT, "tools", "segment_dag_sim.py"))
+    sim = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sim)
+    for rows in (1, 31, 32, 33, 64, 65, 100, 300):
+        for cols in (1, 2, 3, 31, 32, 33, 100):
+            for L in (32, 64, 96, 256):
+                for slots in (1, 2, 5):
+                    sim.simulate(rows, cols, 5, slots, 32, L)
