@@ -468,7 +468,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     SK_CUDA(c.wd.ensure(8 * sizeof(unsigned long long)));
     SK_CUDA(cudaMemsetAsync(c.wd.p, 0, 8 * sizeof(unsigned long long), c.stream()));
     if (bands > 1) SK_CUDA(c.abuf.ensure(slots * col_bytes));
-    const int seg_here = seg_cols;
+    // the DAG's lane-state records (slots x bands x ~5 KB) must fit next to
+    // the column buffers; otherwise this launch streams
+    const size_t rec_bytes = slots * static_cast<size_t>(bands) * susp_record_doubles(ntempl) * sizeof(double);
+    const int seg_here = seg_cols > 0 && rec_bytes <= free_b / 4 ? seg_cols : 0;
     if (seg_here > 0) {
       const size_t nrec = slots * static_cast<size_t>(bands);
       SK_CUDA(c.susp.ensure(nrec * static_cast<size_t>(susp_record_doubles(ntempl)) * sizeof(double)));
