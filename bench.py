@@ -289,7 +289,7 @@ def main():
     flops_per_launch = stats["tile_flops"] / max(1, stats["sweep_launches"])
     achieved = flops_per_launch / (avg_launch_ms / 1e3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "sweep_traffic_r02.json")
+    prof = os.path.join(ROOT, "profiles", "sweep_traffic_r01.json")
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
