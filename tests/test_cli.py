@@ -209,3 +209,19 @@ def test_validate_oracles_agree_with_the_restatement(tmp_path, restatement):
         assert abs(lw - sig) / abs(sig) < 1e-12
         assert abs(fd - want) / abs(want) < 1e-4
         assert abs(pic - want) / abs(want) < 1e-2
+
+
+@pytest.mark.gpu
+def test_kernel_config_file_and_flag_override(tmp_path):
+    """--config supplies option values; a flag given on the command line wins
+    (tools/main.cpp:58-68)."""
+    p = tmp_path / "unit.csv"
+    p.write_text("0\n1\n")
+    cfg = tmp_path / "c.json"
+    cfg.write_text('{"order": 3}')
+    r = run("kernel", p, p, "--config", cfg, "--json")
+    assert r.returncode == 0, r.stderr
+    assert json.loads(r.stdout.strip().splitlines()[1])["order"] == 3
+    assert abs(float(r.stdout.split("=")[1].split()[0]) - (1 + 1 + 1 / 4 + 1 / 36)) < 1e-15
+    r = run("kernel", p, p, "--config", cfg, "--order", 24)
+    assert abs(float(r.stdout.split("=")[1]) - 2.2795853023360673) < 1e-13
