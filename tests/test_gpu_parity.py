@@ -432,3 +432,33 @@ def test_gram_over_a_device_list_matches_one_call(sk, restatement):
     assert list(two.orders) == list(one.orders)
     assert two.max_abs_increment_product == one.max_abs_increment_product
     assert two.orders_converged == one.orders_converged
+
+
+def test_baseline_size_batch_properties(sk, restatement):
+    """BASELINE config 2 at full size (256 pairs, l = 4096, d = 8, adaptive)
+    through the throughput schedule: four pairs against the restatement, and
+    size-independent properties over all 256 -- symmetry K(x,y) = K(y,x) and
+    batch == single-pair evaluation."""
+    xs = np.stack([restatement.brownian(4096, 8, 2 * p + 1) for p in range(256)])
+    ys = np.stack([restatement.brownian(4096, 8, 2 * p + 2) for p in range(256)])
+    pol = sk.TruncationPolicy.adaptive(1e-12)
+    fwd = sk.pairwise(xs, ys, pol)
+    rev = sk.pairwise(ys, xs, pol)
+    assert not fwd.failures and list(fwd.orders) == [8] * 256
+    assert np.max(np.abs(fwd.values - rev.values) / np.maximum(1.0, np.abs(fwd.values))) < 1e-12
+    for p in (0, 77, 255):
+        assert rel(sk.propagate_with_policy(xs[p], ys[p], pol).value, fwd.values[p]) < 1e-13
+    for p in (0, 1, 128, 255):
+        v_ref, _ = restatement.propagate(xs[p], ys[p], 8)
+        assert rel(fwd.values[p], v_ref) < TOL, p
+
+
+def test_long_pair_prefix_identity_at_scale(sk, restatement):
+    """A 65537 x 65537 pair (4.3e9 tiles, the long-pair schedule): knots K(a, a)
+    from the one run equal separate runs on the length-(a+1) prefixes."""
+    x = restatement.brownian(65537, 4, 11)
+    y = restatement.brownian(65537, 4, 12)
+    r = sk.propagate(x, y, 8, diag=True)
+    assert r.diag[-1] == r.value and np.all(np.isfinite(r.diag))
+    for a in (4096, 16384, 40000):
+        assert rel(r.diag[a - 1], sk.propagate(x[: a + 1], y[: a + 1], 8).value) < 1e-12, a
