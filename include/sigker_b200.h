@@ -146,6 +146,9 @@ int sk_exchange_free(void* abuf, void* prog);
 int sk_ipc_handle(void* dptr, void* handle64, sk_status* st);
 int sk_ipc_open(const void* handle64, void** dptr, sk_status* st);
 int sk_ipc_close(void* dptr);
+/* One process driving several GPUs: enable the calling thread's device to
+ * access `peer`'s memory, then pass exchange buffers as plain pointers. */
+int sk_enable_peer_access(int peer, sk_status* st);
 int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
                        uint32_t flags, size_t band_begin, size_t band_end, const void* in_abuf,
                        const void* in_prog, void* out_abuf, void* out_prog, double* value, double* diag,

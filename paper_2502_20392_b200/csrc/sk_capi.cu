@@ -1167,6 +1167,26 @@ int sk_ipc_close(void* dptr) {
   return SK_OK;
 }
 
+// In-process alternative to IPC: let the calling thread's device read and
+// write `peer`'s memory directly (one process driving several GPUs).
+int sk_enable_peer_access(int peer, sk_status* st) {
+  clear_status(st);
+  Ctx* c = nullptr;
+  if (int rc = get_ctx(&c, st)) return rc;
+  if (peer == c->device) return SK_OK;
+  int can = 0;
+  SK_CUDA(cudaDeviceCanAccessPeer(&can, c->device, peer));
+  if (!can)
+    return set_status(st, SK_CUDA_ERROR, 0, 0, "GPU %d cannot access GPU %d's memory (no peer path)", c->device, peer);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return SK_OK;
+  }
+  SK_CUDA(e);
+  return SK_OK;
+}
+
 // One strip of a long pair: bands [band_begin, band_end) of the 32R-row bands
 // (sk_strip_bands).  The bottom band (band_begin > 0) reads its alpha from
 // in_abuf / in_prog (device memory of this GPU, written by the previous

@@ -220,3 +220,90 @@ def strip_bands(ly: int, order: int) -> int:
     if _capi.load().sk_strip_bands(ly, int(order), ctypes.byref(nb)) != 0:
         raise ValueError("bad length/order")
     return nb.value
+
+
+def propagate_long_pair_devices(x, y, order: int, devices: Sequence[int],
+                                options: Optional[sk.PropagateOptions] = None, diag: bool = False):
+    """K(1,1) of ONE long pair split into row strips over several GPUs driven
+    from this process (the SURVEY.md section 8b device-list option; the
+    multi-process variant is propagate_long_pair_distributed).  Strip g runs
+    on devices[g] in its own host thread; its top band writes alpha' straight
+    into devices[g+1]'s exchange buffer through peer access (NVLink), with the
+    same system-scope release/acquire protocol.  Returns (value, diag-or-None).
+    The devices must be distinct: strips wait on each other, so two of them
+    must never share a GPU (one GPU: sk.propagate)."""
+    import threading
+
+    devices = [int(d) for d in devices]
+    if len(set(devices)) != len(devices):
+        raise ValueError("propagate_long_pair_devices: devices must be distinct (strips wait on each other)")
+    x, y = sk._as_series(x), sk._as_series(y)
+    if len(devices) <= 1:
+        lib = _capi.load()
+        if devices:
+            st = _capi.SkStatus()
+            sk._check(lib.sk_set_device(devices[0], ctypes.byref(st)), st)
+        r = sk.propagate(x, y, order, options, diag=diag)
+        return r.value, (r.diag if diag else None)
+    if x.dim() != y.dim():
+        raise ValueError("propagate: series dimensions differ")
+    lib = _capi.load()
+    lx, ly, d = x.length(), y.length(), x.dim()
+    world = len(devices)
+    bands = strip_bands(ly, order)
+    if bands < world:
+        raise ValueError(f"{bands} bands cannot feed {world} GPUs")
+    ranges = strip_ranges(bands, world)
+    st = _capi.SkStatus()
+    xbuf = [None] * world  # exchange buffer (abuf, prog) on each consumer device
+    try:
+        for g in range(1, world):
+            sk._check(lib.sk_set_device(devices[g], ctypes.byref(st)), st)
+            a, p = ctypes.c_void_p(), ctypes.c_void_p()
+            sk._check(lib.sk_exchange_alloc(lx, int(order), ctypes.byref(a), ctypes.byref(p), ctypes.byref(st)), st)
+            xbuf[g] = (a, p)
+        for g in range(world - 1):
+            sk._check(lib.sk_set_device(devices[g], ctypes.byref(st)), st)
+            sk._check(lib.sk_enable_peer_access(devices[g + 1], ctypes.byref(st)), st)
+        xv, yv = x.values(), y.values()
+        out = [None] * world
+        dg = np.full(min(lx, ly) - 1, np.nan) if diag else None
+        parts = [np.full(min(lx, ly) - 1, np.nan) if diag else None for _ in range(world)]
+
+        def strip(g):
+            s = _capi.SkStatus()
+            v = ctypes.c_double(float("nan"))
+            rc = lib.sk_set_device(devices[g], ctypes.byref(s))
+            if rc == 0:
+                b0, b1 = ranges[g]
+                rc = lib.sk_propagate_strip(sk._ptr(xv), lx, sk._ptr(yv), ly, d, int(order), sk._flags(options), b0, b1,
+                                            xbuf[g][0] if g > 0 else None, xbuf[g][1] if g > 0 else None,
+                                            xbuf[g + 1][0] if g + 1 < world else None,
+                                            xbuf[g + 1][1] if g + 1 < world else None, ctypes.byref(v),
+                                            sk._ptr(parts[g]) if diag else None, ctypes.byref(s))
+            out[g] = (rc, s, v.value)
+
+        threads = [threading.Thread(target=strip, args=(g,)) for g in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    finally:
+        for g in range(1, world):
+            if xbuf[g] is not None:
+                lib.sk_exchange_free(xbuf[g][0], xbuf[g][1])
+    recs = [None if rc == 0 else (int(s.code), int(s.tile_k), int(s.tile_l), s.message.decode(errors="replace"))
+            for rc, s, _ in out]
+    err = first_error(recs)
+    if err is not None:
+        code, k, l, msg = err
+        if code == _capi.SK_NUMERIC_OVERFLOW:
+            raise sk.NumericOverflowError(msg, k, l)
+        if code == _capi.SK_INCONSISTENT_BOUNDARY:
+            raise sk.InconsistentBoundaryError(msg)
+        raise RuntimeError(msg)
+    if diag:
+        for g in range(world):
+            sel = ~np.isnan(parts[g])
+            dg[sel] = parts[g][sel]
+    return out[-1][2], dg

@@ -462,3 +462,18 @@ def test_long_pair_prefix_identity_at_scale(sk, restatement):
     assert r.diag[-1] == r.value and np.all(np.isfinite(r.diag))
     for a in (4096, 16384, 40000):
         assert rel(r.diag[a - 1], sk.propagate(x[: a + 1], y[: a + 1], 8).value) < 1e-12, a
+
+
+def test_long_pair_devices_single_gpu_is_plain_propagate(sk, restatement):
+    """propagate_long_pair_devices with one device is the ordinary sweep; with
+    several distinct GPUs it runs the strip pipeline over peer access (not
+    reachable on a one-GPU box -- the protocol itself is pinned by
+    test_strip_protocol_emulated_on_one_gpu)."""
+    from paper_2502_20392_b200 import _capi, distributed as skd
+    x = restatement.brownian(300, 3, 5)
+    y = restatement.brownian(260, 3, 6)
+    v, dg = skd.propagate_long_pair_devices(x, y, 8, devices=[0], diag=True)
+    r = sk.propagate(x, y, 8, diag=True)
+    assert v == r.value and np.array_equal(dg, r.diag)
+    st = _capi.SkStatus()
+    assert _capi.load().sk_enable_peer_access(0, __import__("ctypes").byref(st)) == 0  # own device: no-op

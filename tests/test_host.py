@@ -232,3 +232,12 @@ def test_segment_dag_model():
             for L in (32, 64, 96, 256):
                 for slots in (1, 2, 5):
                     sim.simulate(rows, cols, 5, slots, 32, L)
+
+
+def test_long_pair_devices_rejects_a_shared_gpu():
+    """Strips wait on each other: two strips on one GPU are refused up front
+    (no GPU needed to reach the check)."""
+    from paper_2502_20392_b200 import distributed as skd
+    x = np.cumsum(np.ones((40, 2)), axis=0)
+    with pytest.raises(ValueError, match="distinct"):
+        skd.propagate_long_pair_devices(x, x, 8, devices=[0, 0])
