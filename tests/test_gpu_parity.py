@@ -477,3 +477,40 @@ def test_long_pair_devices_single_gpu_is_plain_propagate(sk, restatement):
     assert v == r.value and np.array_equal(dg, r.diag)
     st = _capi.SkStatus()
     assert _capi.load().sk_enable_peer_access(0, __import__("ctypes").byref(st)) == 0  # own device: no-op
+
+
+def _fd_knots(x, y, R):
+    """Independent check: K_st = rho K on the tile grid by an implicit
+    trapezoidal finite-difference march (R cells per tile), Richardson
+    extrapolated from R and 2R, sampled at the knots."""
+    dx, dy = np.diff(x, axis=0), np.diff(y, axis=0)
+    rho = dy @ dx.T  # rows (y) x cols (x)
+
+    def march(r):
+        rows, cols = rho.shape
+        K = np.ones((cols * r + 1, rows * r + 1))
+        h2 = 1.0 / (r * r)
+        for a in range(cols * r):
+            for b in range(rows * r):
+                q = 0.25 * rho[b // r, a // r] * h2
+                K[a + 1, b + 1] = (K[a + 1, b] + K[a, b + 1] - K[a, b] + q * (K[a, b] + K[a + 1, b] + K[a, b + 1])) / (1 - q)
+        return K[::r, ::r]
+
+    c, f = march(R), march(2 * R)
+    return f + (f - c) / 3.0
+
+
+def test_grid_against_finite_differences(sk, restatement):
+    """test_wavefront.cpp:168-198: the knot grid against an FD solve (R = 16,
+    extrapolated) and the grid's boundary / self-grid symmetry contract."""
+    rng = restatement.rng(808)
+    x = rng.random_series(6, 2, 0.9)
+    y = rng.random_series(5, 2, 0.9)
+    g = sk.propagate_grid(x, y, 24)
+    G = np.asarray(g.grid).reshape(g.grid_rows, g.grid_cols)
+    assert G.shape == (6, 5) and np.all(G[0] == 1.0) and np.all(G[:, 0] == 1.0)
+    fd = _fd_knots(x, y, 16)
+    assert np.max(np.abs(G - fd)) < 2e-4
+    s = sk.propagate_grid(x, x, 24)
+    S = np.asarray(s.grid).reshape(s.grid_rows, s.grid_cols)
+    assert np.max(np.abs(S - S.T)) < 1e-12
