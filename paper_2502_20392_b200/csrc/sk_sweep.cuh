@@ -163,9 +163,13 @@ __host__ __device__ constexpr int ring_stride(int DP) { return DP <= 2 ? 2 : DP 
 // per warp: band-below alpha stage (2 groups) | lane-to-lane alpha slots
 // (32 R) | lane 31's top-row outputs of the chunk | dx ring (DP > 0) | delta
 // stage (R x chunk x 32; x2 for the asynchronously staged table, DP = 0)
+// d = 9..16 (DP = 16): the top lane stores its alpha' straight to global
+// memory instead of parking a chunk of them in shared memory, which keeps the
+// per-warp stage under 1/12 of the SM's shared memory (12 warps resident)
+__host__ __device__ constexpr bool direct_top_out(int DP) { return DP == 16; }
 __host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP) {
   return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + 32 * rows_per_lane(N) * col_stride(N) +
-         chunk_cols(rows_per_lane(N)) * col_stride(N) +
+         (direct_top_out(DP) ? 0 : chunk_cols(rows_per_lane(N)) * col_stride(N)) +
          (DP > 0 ? ring_rows(rows_per_lane(N)) * ring_stride(DP) : 0) +
          (DP > 0 ? 1 : 2) * rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32;
 }
@@ -321,7 +325,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   double* s_alpha = smem;                                   // 2 x K x NP
   double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
   double* s_out = s_pass + 32 * R * NP;                     // K x NP
-  double* s_ring = s_out + kStage;                          // RING x XS (DP > 0)
+  double* s_ring = s_out + (direct_top_out(DP) ? 0 : kStage);  // RING x XS (DP > 0)
   double* s_delta = s_ring + (DP > 0 ? RING * XS : 0);      // [buf][r][k][lane]
   const int n = N > 0 ? N + 1 : P.order + 1;
   const int rows = P.rows, cols = P.cols;
@@ -540,7 +544,19 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       }
       // alpha' up: the band's top row (lane 31, last tile) parks it for the
       // band above, every other row in its slot
-      sts_series<NA>((r == R - 1 && lane == 31) ? s_out + k * NP : s_pass + (32 * r + lane) * NP, qo, n);
+      if constexpr (direct_top_out(DP)) {
+        // every row in its slot (the top lane's slot is never read); the top
+        // row's alpha' straight to the column buffer of the band above
+        sts_series<NA>(s_pass + (32 * r + lane) * NP, qo, n);
+        if (r == R - 1) {
+          const bool up = has_above && lane == 31 && j >= 0 && j < cols;
+          double* dst = out_buf + static_cast<size_t>(up ? j : 0) * NP;
+#pragma unroll
+          for (int m = 0; m < NA; m += 2) st_global_cg2_if(up, dst + m, qo[m], m + 1 < NA ? qo[m + 1] : 0.0);
+        }
+      } else {
+        sts_series<NA>((r == R - 1 && lane == 31) ? s_out + k * NP : s_pass + (32 * r + lane) * NP, qo, n);
+      }
 
       const bool active = row_ok[r] && j >= 0 && j < cols;
       // the reference's throw order inside a tile: delta guard (checked when
@@ -670,7 +686,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     // progress every kPublish columns
     if (has_above) {
       const int jfirst = c0 - 31 - 32 * (R - 1);
-      const int pieces = kend * NP / 2;
+      const int pieces = direct_top_out(DP) ? 0 : kend * NP / 2;
       for (int e = lane; e < pieces; e += 32) {
         const int kk = e / (NP / 2);
         const int jj = jfirst + kk;
