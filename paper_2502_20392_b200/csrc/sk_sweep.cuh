@@ -166,7 +166,10 @@ __host__ __device__ constexpr int ring_stride(int DP) { return DP <= 2 ? 2 : DP 
 // d = 9..16 (DP = 16): the top lane stores its alpha' straight to global
 // memory instead of parking a chunk of them in shared memory, which keeps the
 // per-warp stage under 1/12 of the SM's shared memory (12 warps resident)
-__host__ __device__ constexpr bool direct_top_out(int DP) { return DP == 16; }
+#ifndef SK_DIRECT_OUT_MIN_DP
+#define SK_DIRECT_OUT_MIN_DP 16
+#endif
+__host__ __device__ constexpr bool direct_top_out(int DP) { return DP >= SK_DIRECT_OUT_MIN_DP; }
 __host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP) {
   return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + 32 * rows_per_lane(N) * col_stride(N) +
          (direct_top_out(DP) ? 0 : chunk_cols(rows_per_lane(N)) * col_stride(N)) +
