@@ -245,7 +245,7 @@ def test_segment_dag_matches_streaming(sk, restatement, monkeypatch, seg_cols):
     rng = restatement.rng(2024)
     cases = []
     for (lx, ly, d, order) in [(70, 100, 3, 8), (130, 97, 2, 12), (66, 200, 8, 20), (90, 64, 40, 8), (41, 150, 16, 5),
-                               (2, 300, 2, 8), (3, 170, 1, 6)]:
+                               (2, 300, 2, 8), (3, 170, 1, 6), (50, 90, 40, 20), (60, 120, 12, 10)]:
         xs = np.stack([rng.random_series(lx, d, 1.0) for _ in range(5)])
         ys = np.stack([rng.random_series(ly, d, 1.0) for _ in range(5)])
         cases.append((xs, ys, order))
@@ -409,14 +409,15 @@ def test_strip_protocol_emulated_on_one_gpu(sk, restatement):
     """The long-pair strip hand-off (system-scope release/acquire through an
     exchange buffer) inside one launch: bit-identical to the plain sweep."""
     from paper_2502_20392_b200.distributed import propagate_split_emulated, strip_bands
-    x = restatement.brownian(300, 4, 5)
-    y = restatement.brownian(400, 4, 6)
-    for order in (8, 20):
-        plain = sk.propagate(x, y, order).value
-        nb = strip_bands(400, order)
-        assert nb >= 3
-        for split in range(1, nb):
-            assert propagate_split_emulated(x, y, order, split) == plain, (order, split)
+    for d in (4, 12, 40):  # register kernel with shared-memory / direct top-row hand-up, table path
+        x = restatement.brownian(300, d, 5)
+        y = restatement.brownian(400, d, 6)
+        for order in (8, 20):
+            plain = sk.propagate(x, y, order).value
+            nb = strip_bands(400, order)
+            assert nb >= 3
+            for split in range(1, nb):
+                assert propagate_split_emulated(x, y, order, split) == plain, (d, order, split)
 
 
 def test_gram_over_a_device_list_matches_one_call(sk, restatement):
