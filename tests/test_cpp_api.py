@@ -23,6 +23,17 @@ def test_cpp_api_builds_and_links():
     assert os.path.exists(EXE)
 
 
+def test_thread_pool_drop_in():
+    """host-only part of the drop-in (no GPU work): runs on the CPU"""
+    exe = os.path.join(ROOT, "build", "test_thread_pool")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_thread_pool.cpp"), "-o", exe, "-L", PKG, "-lsigker",
+                    "-lsigker_b200", f"-Wl,-rpath,{PKG}", "-lpthread"], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+
+
 @pytest.mark.gpu
 def test_cpp_api_suite():
     build()
