@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SK_ABI_VERSION 1
+#define SK_ABI_VERSION 2
 
 /* Status codes (errors.hpp:10-53 of the reference). */
 enum sk_code {
@@ -132,6 +132,11 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
  * because the family is padded to one length).  Host arithmetic only. */
 int sk_gram_shard_range(size_t m, size_t shard, size_t nshards, size_t* first, size_t* last);
 
+/* 1 when every one of the n doubles is finite, else 0 (the TimeSeries
+ * constructor's check, time_series.cpp:9-19): a branch-free exponent test,
+ * split over host threads for large inputs.  Host memory, host work only. */
+int sk_all_finite(const double* v, size_t n);
+
 /* ---- Multi-GPU long pair: strip pipeline (cfg 3).
  * The ly-1 tile rows are cut into bands of 32*R rows (sk_strip_bands); GPU g
  * sweeps a contiguous band range and hands its top band's alpha series to
@@ -169,6 +174,7 @@ typedef struct sk_stats {
   double tile_flops;       /* algorithmic FP64 flops, sum of F(N,d) per tile */
   uint64_t table_launches; /* rho-table builds (d > 16: DMMA GEMM)        */
   double table_ms;         /* summed device time of those builds          */
+  uint64_t paired_launches; /* sweep launches with two-warp (paired) bands (ABI 2) */
 } sk_stats;
 
 int sk_stats_enable(int enable);

@@ -4,6 +4,8 @@
 // initialisation and single-tile entry points.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "sk_device.cuh"
@@ -33,27 +35,46 @@ __global__ void increments_kernel(const double* __restrict__ v, size_t nseries, 
   }
 }
 
-// Per series: max_k sum_c dz_k[c]^2 (only feeds the Cauchy-Schwarz upper
-// bound of max|rho|, so its rounding is covered by the bound's slack).
-__global__ void max_sqnorm_kernel(const double* __restrict__ inc, size_t count, size_t dim, size_t ld,
-                                  double* __restrict__ out) {
-  const double* s = inc + blockIdx.x * (count + 1) * ld + ld;
+// Per series: max_k sum_c dz_k[c]^2 (feeds the Cauchy-Schwarz upper bound of
+// max|rho| and the fast-dot error bound of the exact-order path; its rounding
+// is covered by their slack).  `bps` blocks per series, rows strided across
+// them; out[] holds the bits of a nonnegative double, zeroed by the launcher,
+// so atomicMax on the bits is the max of the values.  d <= 16: a thread per
+// row, coordinates in order; d > 16: a warp per row, lanes over coordinates
+// (coalesced rows of ld doubles).
+template <bool WARP_ROW>
+__global__ void max_sqnorm_kernel(const double* __restrict__ inc, size_t count, size_t dim, size_t ld, int bps,
+                                  unsigned long long* __restrict__ out) {
+  const size_t series = blockIdx.x / bps, part = blockIdx.x - series * bps;
+  const double* s = inc + series * (count + 1) * ld + ld;
+  const int lane = threadIdx.x & 31;
   double best = 0.0;
-  for (size_t k = threadIdx.x; k < count; k += blockDim.x) {
-    double acc = 0.0;
-    for (size_t c = 0; c < dim; ++c) acc = fma(s[k * ld + c], s[k * ld + c], acc);
-    best = fmax(best, acc);
+  if constexpr (WARP_ROW) {
+    const size_t wpb = blockDim.x >> 5;
+    for (size_t k = part * wpb + (threadIdx.x >> 5); k < count; k += bps * wpb) {
+      double acc = 0.0;
+      for (size_t c = lane; c < dim; c += 32) acc = fma(s[k * ld + c], s[k * ld + c], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      best = fmax(best, acc);
+    }
+  } else {
+    for (size_t k = part * blockDim.x + threadIdx.x; k < count; k += static_cast<size_t>(bps) * blockDim.x) {
+      double acc = 0.0;
+      for (size_t c = 0; c < dim; ++c) acc = fma(s[k * ld + c], s[k * ld + c], acc);
+      best = fmax(best, acc);
+    }
   }
   __shared__ double red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  if (lane == 0) red[threadIdx.x >> 5] = best;
   __syncthreads();
   if (threadIdx.x < 32) {
     best = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if (threadIdx.x == 0) out[blockIdx.x] = best;
+    if (threadIdx.x == 0 && best > 0.0) atomicMax(out + series, static_cast<unsigned long long>(__double_as_longlong(best)));
   }
 }
 
@@ -275,7 +296,19 @@ cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_
 cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, size_t ld, double* out,
                               cudaStream_t st) {
   if (nseries == 0) return cudaSuccess;
-  max_sqnorm_kernel<<<static_cast<unsigned>(nseries), 256, 0, st>>>(inc, count, dim, ld, out);
+  cudaError_t e = cudaMemsetAsync(out, 0, nseries * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  const bool warp_row = dim > 16;
+  const size_t rows_per_block = warp_row ? 8 : 256;
+  const size_t want = (count + rows_per_block - 1) / rows_per_block;
+  const size_t cap = std::max<size_t>(1, 148 * 16 / nseries);
+  const int bps = static_cast<int>(std::max<size_t>(1, std::min(want, cap)));
+  const unsigned blocks = static_cast<unsigned>(nseries * bps);
+  auto* bits = reinterpret_cast<unsigned long long*>(out);
+  if (warp_row)
+    max_sqnorm_kernel<true><<<blocks, 256, 0, st>>>(inc, count, dim, ld, bps, bits);
+  else
+    max_sqnorm_kernel<false><<<blocks, 256, 0, st>>>(inc, count, dim, ld, bps, bits);
   return cudaGetLastError();
 }
 
@@ -308,11 +341,16 @@ cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint3
                                                          tab_stride);
     return cudaGetLastError();
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(rho_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  // function attributes are per device: set once on each device used
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(rho_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   const dim3 grid((cols + kGT - 1) / kGT, (rows + kGT - 1) / kGT, static_cast<unsigned>(npairs));
   rho_gemm_kernel<<<grid, 128, kGemmSmem, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, ld, tab, tab_stride);

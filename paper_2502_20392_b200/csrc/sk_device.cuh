@@ -99,13 +99,11 @@ __host__ __device__ constexpr double kFactRatio(int m) {
 // N = 8) still need three vector operands.  Returns total.  `fault` flips
 // the sign of the W[1][1] contribution (the reference's negative-control
 // hook, tile_series.cpp:51-52).
+// ph[m] = delta^m / N! by a depth-4 product tree (d2 = delta^2, d4 = delta^4);
+// p[m] = delta^m / m! = ph[m] * (N!/m!), an integer immediate multiplier
 template <int N>
-__device__ __forceinline__ void tile_update_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
-                                                   double (&qo)[N + 1], double (&ro)[N + 1], bool fault) {
+__device__ __forceinline__ void tile_powers(double delta, double (&ph)[N + 1], double (&p)[N + 1]) {
   constexpr int n = N + 1;
-  // ph[m] = delta^m / N! by a depth-4 product tree (d2 = delta^2, d4 = delta^4);
-  // p[m] = delta^m / m! = ph[m] * (N!/m!), an integer immediate multiplier
-  double ph[n], p[n];
   ph[0] = c_inv_fact[N];
   p[0] = 1.0;
   if constexpr (N >= 1) {
@@ -125,6 +123,77 @@ __device__ __forceinline__ void tile_update_scaled(const double (&q)[N + 1], con
 #pragma unroll
     for (int m = 2; m < n; ++m) p[m] = ph[m] * kFactRatio<N>(m);
   }
+}
+
+// alpha' alone (the paired-band kernel's alpha warp), powers precomputed
+// (tile_powers): the same expressions, in the same order, as
+// tile_update_scaled, so the bits are identical
+template <int N>
+__device__ __forceinline__ void tile_alpha_scaled(const double (&q)[N + 1], const double (&r)[N + 1],
+                                                  const double (&ph)[N + 1], const double (&p)[N + 1], double delta,
+                                                  double (&qo)[N + 1], bool fault) {
+  constexpr int n = N + 1;
+  double v[N > 0 ? N : 1];
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    double acc = r[1];
+#pragma unroll
+    for (int k = 2; k <= N - a; ++k) acc = fma(acc, static_cast<double>(a + k), r[k]);
+    v[a] = acc;
+  }
+#pragma unroll
+  for (int a = 0; a < n; ++a) qo[a] = q[a];
+#pragma unroll
+  for (int b = 1; b < n; ++b)
+#pragma unroll
+    for (int a = b; a < n; ++a) qo[a] = fma(q[a - b], p[b], qo[a]);
+#pragma unroll
+  for (int a = 0; a < N; ++a) qo[a] = fma(ph[a], v[a], qo[a]);
+  if constexpr (N >= 1) {
+    if (fault) {
+      const double c11 = 2.0 * q[0] * delta;
+      qo[1] -= c11;
+    }
+  }
+}
+
+// beta' alone (the paired-band kernel's beta warp), bit-identical likewise
+template <int N>
+__device__ __forceinline__ void tile_beta_scaled(const double (&q)[N + 1], const double (&r)[N + 1],
+                                                 const double (&ph)[N + 1], const double (&p)[N + 1], double delta,
+                                                 double (&ro)[N + 1], bool fault) {
+  constexpr int n = N + 1;
+  double u[n];
+#pragma unroll
+  for (int b = 0; b < n; ++b) {
+    double acc = q[0];
+#pragma unroll
+    for (int k = 1; k <= N - b; ++k) acc = fma(acc, static_cast<double>(b + k), q[k]);
+    u[b] = acc;
+  }
+#pragma unroll
+  for (int c = 1; c < n; ++c) ro[c] = r[c];
+#pragma unroll
+  for (int b = 1; b < n; ++b)
+#pragma unroll
+    for (int c = b + 1; c < n; ++c) ro[c] = fma(r[c - b], p[b], ro[c]);
+  ro[0] = ph[0] * u[0];
+#pragma unroll
+  for (int b = 1; b < n; ++b) ro[b] = fma(ph[b], u[b], ro[b]);
+  if constexpr (N >= 1) {
+    if (fault) {
+      const double c11 = 2.0 * q[0] * delta;
+      ro[1] -= c11;
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void tile_update_scaled(const double (&q)[N + 1], const double (&r)[N + 1], double delta,
+                                                   double (&qo)[N + 1], double (&ro)[N + 1], bool fault) {
+  constexpr int n = N + 1;
+  double ph[n], p[n];
+  tile_powers<N>(delta, ph, p);
   // Hankel parts by integer Horner recurrences (immediate multipliers)
   double u[n], v[N > 0 ? N : 1];
 #pragma unroll

@@ -51,8 +51,11 @@ cudaError_t launch_step_tile_fast(double delta, int order, const double* in, dou
 // exact: reference-identical delta (sequential non-FMA dot) + per-pair
 // max|delta| tracking; otherwise an FMA dot and no max tracking.
 // extras: knot grid / diagonal outputs.
-cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, int grid, cudaStream_t stream,
+// paired: two-warp bands (alpha warp + beta warp per band; streaming schedule,
+// register kernels, no exact max) for launches that leave most SM
+// sub-partitions idle: about half the per-step latency of a one-warp band.
+cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream,
                          const SweepParams& P);
-cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, int* blocks_per_sm);
+cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
 
 }  // namespace skb

@@ -89,11 +89,8 @@ class TimeSeries:
             raise ValueError("time series must contain at least one point")
         if v.size % dim != 0:
             raise ValueError("value count is not a multiple of the dimension")
-        # time_series.cpp:9-19.  A finite sum proves every value finite (NaN and
-        # inf propagate); only an overflowing sum needs the elementwise test
-        with np.errstate(over="ignore", invalid="ignore"):
-            total = float(v.sum())
-        if not (math.isfinite(total) or np.all(np.isfinite(v))):
+        # time_series.cpp:9-19 (sk_all_finite: threaded exponent test on the host)
+        if not _capi.load().sk_all_finite(v.ctypes.data, v.size):
             raise ValueError("time series coordinates must be finite")
         self._v = v.reshape(-1, dim)
         self._v.setflags(write=False)
@@ -625,4 +622,4 @@ def stats_get() -> dict:
     _capi.load().sk_stats_get(ctypes.byref(s))
     return {"sweep_launches": s.sweep_launches, "aux_launches": s.aux_launches, "sweep_ms": s.sweep_ms,
             "tiles": s.tiles, "tile_flops": s.tile_flops, "table_launches": s.table_launches,
-            "table_ms": s.table_ms}
+            "table_ms": s.table_ms, "paired_launches": s.paired_launches}

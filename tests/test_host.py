@@ -35,7 +35,7 @@ def test_capi_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", _capi.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (sk_[a-z_0-9]+)$", out, re.M))
     assert set(declared) <= exported
-    assert lib.sk_abi_version() == 1
+    assert lib.sk_abi_version() == 2
 
 
 def test_estimate_order_matches_reference_table():
@@ -99,6 +99,26 @@ def test_time_series_contract():
     assert tab.rho(1, 0) == 4.0
     with pytest.raises(ValueError):
         tab.rho(2, 0)
+
+
+def test_all_finite_scan():
+    """sk_all_finite (the TimeSeries check) on the threaded and the serial path:
+    one non-finite value anywhere -- first, last, chunk seams -- is found."""
+    from paper_2502_20392_b200 import _capi, sigker as sk
+    lib = _capi.load()
+    for n in (1, 7, (1 << 20) + 3, 5 * (1 << 20) + 11):
+        v = np.random.default_rng(n).standard_normal(n)
+        assert lib.sk_all_finite(v.ctypes.data, n) == 1
+        for pos in sorted({0, n - 1, n // 2, min(n - 1, 1 << 20), min(n - 1, (1 << 20) - 1)}):
+            for bad in (np.nan, np.inf, -np.inf):
+                w = v.copy()
+                w[pos] = bad
+                assert lib.sk_all_finite(w.ctypes.data, n) == 0, (n, pos, bad)
+    big = np.zeros((1 << 21, 2))
+    big[-1, 1] = np.inf
+    with pytest.raises(ValueError):
+        sk.TimeSeries(big)
+    assert lib.sk_all_finite(np.full(4, 1.7976931348623157e308).ctypes.data, 4) == 1
 
 
 def test_propagate_argument_validation():
