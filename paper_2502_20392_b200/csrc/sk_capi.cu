@@ -431,15 +431,15 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / (static_cast<size_t>(bands) * spb)));
   }
 
-  // Paired bands (sweep_pair_kernel): a streaming launch whose one-warp bands
-  // leave most SM sub-partitions idle (one pair up to ~9000 points, a few
-  // short pairs) runs every band on two warps, alpha' and beta' split between
-  // them (the same bits; ~15 % less per-step latency, measured).  Every warp
-  // of the launch must have a sub-partition to itself: a shared one slows its
-  // band, and every band above it waits.
+  // Paired bands (sweep_pair_kernel, SK_PAIRED=1): every band of a streaming
+  // launch on two warps, alpha' and beta' split between them (the same bits).
+  // Opt-in: with tile totals formed only where a final tile can fall
+  // (kFlagAllTotals) the one-warp band has the shorter step (measured at
+  // l = 1001 / 4097: 552 ns one-warp vs 596 ns paired per wavefront step).
   int pair_bps = 0;
   bool paired = false;
-  if (seg_cols == 0 && whole && !exact && ntempl > 0 && rows_per_lane(ntempl) == 1) {
+  const char* pe = std::getenv("SK_PAIRED");
+  if (pe && pe[0] == '1' && seg_cols == 0 && whole && !exact && ntempl > 0 && rows_per_lane(ntempl) == 1) {
     const int pkey = okey | (1 << 30);
     if (auto it = c.occupancy.find(pkey); it != c.occupancy.end()) {
       pair_bps = it->second;
@@ -447,10 +447,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
       SK_CUDA(sweep_occupancy(ntempl, dp, false, extras, true, &pair_bps));
       c.occupancy[pkey] = pair_bps;
     }
-    const size_t npl = std::min(chunk, npairs_all);
-    paired = pair_bps > 0 && 2 * npl * static_cast<size_t>(bands) <= 4 * static_cast<size_t>(c.sms) &&
-             npl * static_cast<size_t>(bands) <= static_cast<size_t>(pair_bps) * c.sms;
-    if (const char* e = std::getenv("SK_PAIRED")) paired = pair_bps > 0 && e[0] == '1';
+    paired = pair_bps > 0;
   }
 
   for (size_t c0 = 0; c0 < npairs_all; c0 += chunk) {
@@ -549,6 +546,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.group = static_cast<int>(group);
     P.slots = static_cast<int>(slots);
     P.flags = flags;
+    if (const char* e = std::getenv("SK_ALL_TOTALS"); e && e[0] == '1') P.flags |= kFlagAllTotals;
     P.abuf = bands > 1 ? c.abuf.as<double>() : nullptr;
     P.prog = c.prog.as<unsigned long long>();
     P.queue = c.queue.as<unsigned>();
@@ -671,6 +669,41 @@ int decode_err(unsigned long long key, sk_status* st, const double* xinc_host, c
                     static_cast<unsigned long long>(j + 1), static_cast<unsigned long long>(i + 1));
 }
 
+// Throughput sweeps form tile totals only where a pair's final tile can fall
+// (kFlagAllTotals).  A pair that ended flagged (its first failure may be
+// preceded by an unchecked non-finite tile) or non-finite is swept again with
+// every total formed and checked: the reference's first failing tile, exactly.
+// Launch index t writes output slot t (values / err, hv / he on the host).
+int recheck_failures(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const std::vector<uint32_t>& py,
+                     const std::vector<int>& ords, uint32_t flags, const Outputs& o, std::vector<double>& hv,
+                     std::vector<unsigned long long>& he, sk_status* st) {
+  std::vector<uint32_t> redo;
+  for (size_t t = 0; t < he.size(); ++t)
+    if (he[t] != ~0ull || !std::isfinite(hv[t])) redo.push_back(static_cast<uint32_t>(t));
+  if (redo.empty()) return SK_OK;
+  for (uint32_t t : redo) SK_CUDA(cudaMemsetAsync(o.d_err + t, 0xff, sizeof(unsigned long long), c.stream()));
+  std::vector<int> distinct;
+  for (uint32_t t : redo) distinct.push_back(ords[t]);
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  for (int ord : distinct) {
+    std::vector<uint32_t> gx, gy, go;
+    for (uint32_t t : redo)
+      if (ords[t] == ord) {
+        gx.push_back(px[t]);
+        gy.push_back(py[t]);
+        go.push_back(t);
+      }
+    if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags | kFlagAllTotals, o, st)) return rc;
+  }
+  for (uint32_t t : redo) {
+    SK_CUDA(cudaMemcpyAsync(&hv[t], o.d_values + t, sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    SK_CUDA(cudaMemcpyAsync(&he[t], o.d_err + t, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream()));
+  }
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  return SK_OK;
+}
+
 // Pairwise core on device-resident raw series.  values: device, npairs.
 struct PairwiseResult {
   std::vector<int> orders, conv;
@@ -734,8 +767,10 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
   }
   tr.mark("sweep launch (async)");
   res.err.resize(npairs);
+  std::vector<double> hv(npairs);
   SK_CUDA(cudaMemcpyAsync(res.err.data(), c.err.p, npairs * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           c.stream()));
+  SK_CUDA(cudaMemcpyAsync(hv.data(), d_values, npairs * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
   if (want_maxrho) {
     res.maxr.resize(npairs);
     SK_CUDA(cudaMemcpyAsync(res.maxr.data(), c.maxr.p, npairs * sizeof(unsigned long long),
@@ -744,6 +779,9 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
   SK_CUDA(cudaStreamSynchronize(c.stream()));
   SK_CUDA(cudaGetLastError());
   tr.mark("sweep done (sync)");
+  // grid / diagonal sweeps form every total already
+  if (!d_grid && !d_diag)
+    if (int rc = recheck_failures(c, ps, px, py, res.orders, flags, o, hv, res.err, st)) return rc;
   return SK_OK;
 }
 
@@ -1092,6 +1130,7 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
                             c.stream()));
   SK_CUDA(cudaStreamSynchronize(c.stream()));
   SK_CUDA(cudaGetLastError());
+  if (int rc = recheck_failures(c, ps, pi, pj, ords, flags, o, hv, he, st)) return rc;
   double best = 0.0;
   int first_fatal = -1;
   for (size_t t = 0; t < np; ++t) {
@@ -1275,7 +1314,7 @@ int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, s
     s.xout_prog = static_cast<unsigned long long*>(out_prog);
   }
   std::vector<uint32_t> zero(1, 0);
-  if (int rc = run_sweeps(c, ps, zero, zero, zero, order, flags, o, st, s)) return rc;
+  if (int rc = run_sweeps(c, ps, zero, zero, zero, order, flags | kFlagAllTotals, o, st, s)) return rc;
   unsigned long long key = ~0ull;
   SK_CUDA(cudaMemcpyAsync(&key, c.err.p, sizeof key, cudaMemcpyDeviceToHost, c.stream()));
   double v = std::numeric_limits<double>::quiet_NaN();
@@ -1333,7 +1372,7 @@ int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, s
     s.xin_prog = static_cast<const unsigned long long*>(xp);
     s.xout_prog = static_cast<unsigned long long*>(xp);
     std::vector<uint32_t> zero(1, 0);
-    if ((rc = run_sweeps(c, ps, zero, zero, zero, order, flags, o, st, s)) != SK_OK) break;
+    if ((rc = run_sweeps(c, ps, zero, zero, zero, order, flags | kFlagAllTotals, o, st, s)) != SK_OK) break;
     unsigned long long key = ~0ull;
     cudaMemcpyAsync(&key, c.err.p, sizeof key, cudaMemcpyDeviceToHost, c.stream());
     cudaMemcpyAsync(value, c.values.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream());

@@ -33,6 +33,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "sk_device.cuh"
 
@@ -154,6 +155,13 @@ __host__ __device__ inline SegRange seg_range(int rows, int cols, int b, int H, 
 
 constexpr unsigned kFlagStrictCorner = 1u;
 constexpr unsigned kFlagWFault = 4u;
+// Internal: form and check every tile's total.  Without it (throughput
+// launches) a band forms totals only in the chunks that can hold its pair's
+// final tile; a non-finite total anywhere else still reaches the final value
+// (non-finite series propagate through every later tile to the corner), and
+// the host sweeps any pair that ends non-finite or flagged again with this
+// bit set, which reports the reference's first failing tile exactly.
+constexpr unsigned kFlagAllTotals = 1u << 8;
 
 __host__ __device__ constexpr int series_len(int N) { return N > 0 ? N + 1 : kMaxOrder + 1; }
 __host__ __device__ constexpr int col_stride(int N) { return (series_len(N) + 1) & ~1; }
@@ -359,6 +367,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const unsigned out = P.pair_out[p];
   const bool strict = (P.flags & kFlagStrictCorner) != 0;
   const bool fault = (P.flags & kFlagWFault) != 0;
+  const bool all_totals = EXTRAS || N == 0 || (P.flags & kFlagAllTotals) != 0;
+  const bool band_top = row0 + 32 * R >= rows;  // the band holds the pair's last row
   const bool streaming = P.seg_cols == 0;
   // PAIRED: both warps of the band leave together (the alpha warp decides)
   auto agree = [&](bool ok) {
@@ -520,7 +530,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   if (!beta_warp) stage_group(c_begin);
 
   // one step = R tiles of this lane (one basic block, conditional work predicated)
-  auto step = [&](int s, int k, const double* stage, const double* dl, double (&r_in)[R][NA],
+  auto step = [&](bool TOT, int s, int k, const double* stage, const double* dl, double (&r_in)[R][NA],
                   double (&ro_out)[R][NA]) {
     double q[R][NA];
     // alpha: lane 0's first tile from the band below (stage); every other
@@ -558,11 +568,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       double qo[NA];
       double total = 0.0;
       if constexpr (N > 0) {
-        // the total is formed at every tile: the error contract needs it
-        // (non-finite total, wavefront.cpp:169-173).  Measured: skipping it
-        // behind an integer finiteness screen costs more than it saves.
+        // the total (non-finite check, wavefront.cpp:169-173; the final
+        // value) only in TOT chunks -- see kFlagAllTotals
         tile_update_scaled<N>(q[r], r_in[r], delta, qo, ro_out[r], fault);
-        total = scaled_total<N>(qo);
+        if (TOT) total = scaled_total<N>(qo);
       } else {
         total = tile_step_literal(P.order, q[r], r_in[r], delta, P.w65, qo, ro_out[r]);
       }
@@ -587,11 +596,11 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       // the chunk's deltas are formed), corner check, non-finite total
       // (wavefront.cpp:150-173); the first failing tile of the row wins
       const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0]);
-      const bool nf = !isfinite(total);
+      const bool nf = (TOT || N == 0) && !isfinite(total);
       const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
       const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
       jkey[r] = min(jkey[r], (active && code != 0u) ? kk : ~0u);
-      st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
+      if (TOT || N == 0) st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
       if constexpr (EXTRAS) {
         if (P.grid)
           st_global_if(active,
@@ -732,18 +741,29 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       const int kend = min(K, steps - c0);
       form_deltas(c0, kend, dl);
       __syncwarp();
-      int k = 0;
+      auto run_chunk = [&](bool tot) {
+        int k = 0;
 #pragma unroll 1
-      for (; k + 1 < kend; k += 2) {
-        step(c0 + k, k, stage, dl, roA, roB);
-        step(c0 + k + 1, k + 1, stage, dl, roB, roA);
-      }
-      if (k < kend) {
-        step(c0 + k, k, stage, dl, roA, roB);
+        for (; k + 1 < kend; k += 2) {
+          step(tot, c0 + k, k, stage, dl, roA, roB);
+          step(tot, c0 + k + 1, k + 1, stage, dl, roB, roA);
+        }
+        if (k < kend) {
+          step(tot, c0 + k, k, stage, dl, roA, roB);
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+          for (int r = 0; r < R; ++r)
 #pragma unroll
-          for (int m = 0; m < NA; ++m) roA[r][m] = roB[r][m];
+            for (int m = 0; m < NA; ++m) roA[r][m] = roB[r][m];
+        }
+      };
+      // totals where the pair's final tile can fall (or everywhere, kFlagAllTotals)
+      if constexpr (EXTRAS || N == 0) {
+        run_chunk(true);
+      } else {
+        if (all_totals || (band_top && c0 + K > cols - 1))
+          run_chunk(true);
+        else
+          run_chunk(false);
       }
       hand_up(c0, kend);
     }
@@ -769,8 +789,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
         return dl[k * 32 + lane];
       }
     };
-    auto step2 = [&](int s, int k, const double* stage, double delta, const double (&ph)[NA], const double (&pw)[NA],
-                     double (&r_in)[NA], double (&ro_out)[NA]) {
+    auto step2 = [&](bool TOT, int s, int k, const double* stage, double delta, const double (&ph)[NA],
+                     const double (&pw)[NA], double (&r_in)[NA], double (&ro_out)[NA]) {
       const int par = s & 1;
       const double* sp_rd = par ? s_pass2 : s_pass;
       double* sp_wr = par ? s_pass : s_pass2;
@@ -789,7 +809,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
                                      ? (static_cast<unsigned>(j) << 2) | kErrDelta
                                      : ~0u);
         tile_alpha_scaled<N>(q, r, ph, pw, delta, qo, fault);
-        const double total = scaled_total<N>(qo);
+        double total = 0.0;
+        if (TOT) total = scaled_total<N>(qo);
         if constexpr (direct_top_out(DP)) {
           sts_series<NA>(sp_wr + lane * NP, qo, n);
           const bool up = has_above && lane == 31 && j >= 0 && j < cols;
@@ -800,11 +821,11 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           sts_series<NA>(lane == 31 ? s_out + k * NP : sp_wr + lane * NP, qo, n);
         }
         const bool cm = strict & corner_mismatch(q[0], r[0]);
-        const bool nf = !isfinite(total);
+        const bool nf = TOT && !isfinite(total);
         const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
         const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
         jkey[0] = min(jkey[0], (act && code != 0u) ? kk : ~0u);
-        st_global_if(last_row[0] && j == cols - 1, P.values + out, total);
+        if (TOT) st_global_if(last_row[0] && j == cols - 1, P.values + out, total);
         if constexpr (EXTRAS) {
           if (P.grid)
             st_global_if(act, P.grid + out * P.grid_stride + static_cast<size_t>(j + 1) * (rows + 1) + (irow[0] + 1),
@@ -836,25 +857,35 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
         if (!beta_warp) form_deltas(c0, kend, dl);
         __syncthreads();
       }
-      double d0 = delta_at(c0, 0, dl), ph0[NA], pw0[NA];
-      tile_powers<N>(d0, ph0, pw0);
-      int k = 0;
+      auto run_chunk = [&](bool tot) {
+        double d0 = delta_at(c0, 0, dl), ph0[NA], pw0[NA];
+        tile_powers<N>(d0, ph0, pw0);
+        int k = 0;
 #pragma unroll 1
-      for (; k + 1 < kend; k += 2) {
-        const double d1 = delta_at(c0 + k + 1, k + 1, dl);
-        double ph1[NA], pw1[NA];
-        tile_powers<N>(d1, ph1, pw1);
-        step2(c0 + k, k, stage, d0, ph0, pw0, roA[0], roB[0]);
-        if (k + 2 < kend) {
-          d0 = delta_at(c0 + k + 2, k + 2, dl);
-          tile_powers<N>(d0, ph0, pw0);
+        for (; k + 1 < kend; k += 2) {
+          const double d1 = delta_at(c0 + k + 1, k + 1, dl);
+          double ph1[NA], pw1[NA];
+          tile_powers<N>(d1, ph1, pw1);
+          step2(tot, c0 + k, k, stage, d0, ph0, pw0, roA[0], roB[0]);
+          if (k + 2 < kend) {
+            d0 = delta_at(c0 + k + 2, k + 2, dl);
+            tile_powers<N>(d0, ph0, pw0);
+          }
+          step2(tot, c0 + k + 1, k + 1, stage, d1, ph1, pw1, roB[0], roA[0]);
         }
-        step2(c0 + k + 1, k + 1, stage, d1, ph1, pw1, roB[0], roA[0]);
-      }
-      if (k < kend) {
-        step2(c0 + k, k, stage, d0, ph0, pw0, roA[0], roB[0]);
+        if (k < kend) {
+          step2(tot, c0 + k, k, stage, d0, ph0, pw0, roA[0], roB[0]);
 #pragma unroll
-        for (int m = 0; m < NA; ++m) roA[0][m] = roB[0][m];
+          for (int m = 0; m < NA; ++m) roA[0][m] = roB[0][m];
+        }
+      };
+      if constexpr (EXTRAS) {
+        run_chunk(true);
+      } else {
+        if (all_totals || (band_top && c0 + K > cols - 1))
+          run_chunk(true);
+        else
+          run_chunk(false);
       }
       if (!beta_warp) hand_up(c0, kend);
     }

@@ -69,9 +69,10 @@ def test_paired_bands_bit_identical_to_one_warp_bands(sk, restatement, monkeypat
         assert a == b, (k, str(a)[:300], str(b)[:300])
 
 
-def test_paired_bands_chosen_for_a_single_long_pair(sk, restatement):
-    """The default schedule picks paired bands for one long pair and matches
-    the oracle (the reference's algorithm) at the parity tolerance."""
+def test_paired_bands_chosen_for_a_single_long_pair(sk, restatement, monkeypatch):
+    """With SK_PAIRED=1 the schedule picks paired bands for one long pair and
+    matches the oracle (the reference's algorithm) at the parity tolerance."""
+    monkeypatch.setenv("SK_PAIRED", "1")
     x = restatement.brownian(1500, 2, 11)
     y = restatement.brownian(1200, 2, 12)
     sk.stats_enable(True)
