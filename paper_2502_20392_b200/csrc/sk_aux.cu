@@ -35,6 +35,46 @@ __global__ void increments_kernel(const double* __restrict__ v, size_t nseries, 
   }
 }
 
+// The same layout for ld = LD in {2, 4, 8, 16} (d <= 16), one thread per
+// output row (no index divisions: rows of a series along x, series along y),
+// fused with the per-series max_k sum_c dz_k[c]^2 of max_sqnorm_kernel (same
+// FMA order, so the same bits) when `sqn` is set.  Row k + 1 reads input rows
+// k and k + 1; the neighbour's row comes from L1.
+template <int LD>
+__global__ void __launch_bounds__(256) increments_rows_kernel(const double* __restrict__ v, size_t nseries, size_t len,
+                                                              int dim, double* __restrict__ out,
+                                                              unsigned long long* __restrict__ sqn) {
+  const size_t row = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  for (size_t s = blockIdx.y; s < nseries; s += gridDim.y) {
+    double best = 0.0;
+    if (row < len) {
+      double val[LD];
+#pragma unroll
+      for (int c = 0; c < LD; ++c) val[c] = 0.0;
+      if (row > 0) {
+        const double* src = v + (s * len + row - 1) * dim;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < LD; ++c)
+          if (c < dim) {
+            val[c] = src[dim + c] - src[c];
+            acc = fma(val[c], val[c], acc);
+          }
+        best = acc;
+      }
+      double2* dst = reinterpret_cast<double2*>(out + (s * len + row) * LD);
+#pragma unroll
+      for (int c = 0; c < LD; c += 2) dst[c / 2] = make_double2(val[c], val[c + 1]);
+    }
+    if (sqn) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (lane == 0 && best > 0.0) atomicMax(sqn + s, static_cast<unsigned long long>(__double_as_longlong(best)));
+    }
+  }
+}
+
 // Per series: max_k sum_c dz_k[c]^2 (feeds the Cauchy-Schwarz upper bound of
 // max|rho| and the fast-dot error bound of the exact-order path; its rounding
 // is covered by their slack).  `bps` blocks per series, rows strided across
@@ -286,11 +326,28 @@ static int grid_for(size_t work, int threads) {
 }
 
 cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, size_t ld, double* out,
-                              cudaStream_t st) {
+                              cudaStream_t st, double* sqn) {
   const size_t work = nseries * len * ld;
   if (work == 0) return cudaSuccess;
+  if (sqn) {
+    cudaError_t e = cudaMemsetAsync(sqn, 0, nseries * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+  }
+  if (ld == 2 || ld == 4 || ld == 8 || ld == 16) {
+    const dim3 grid(static_cast<unsigned>((len + 255) / 256), static_cast<unsigned>(std::min<size_t>(nseries, 65535)));
+    auto* bits = reinterpret_cast<unsigned long long*>(sqn);
+    const int d = static_cast<int>(dim);
+    switch (ld) {
+      case 2: increments_rows_kernel<2><<<grid, 256, 0, st>>>(v, nseries, len, d, out, bits); break;
+      case 4: increments_rows_kernel<4><<<grid, 256, 0, st>>>(v, nseries, len, d, out, bits); break;
+      case 8: increments_rows_kernel<8><<<grid, 256, 0, st>>>(v, nseries, len, d, out, bits); break;
+      default: increments_rows_kernel<16><<<grid, 256, 0, st>>>(v, nseries, len, d, out, bits); break;
+    }
+    return cudaGetLastError();
+  }
   increments_kernel<<<grid_for(work, 256), 256, 0, st>>>(v, nseries, len, dim, ld, out);
-  return cudaGetLastError();
+  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess || !sqn) return e;
+  return launch_max_sqnorm(out, nseries, len - 1, dim, ld, sqn, st);
 }
 
 cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, size_t ld, double* out,

@@ -719,18 +719,19 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
   const size_t ld = inc_ld(dim);
   SK_CUDA(c.xinc.ensure(npairs * lx * ld * sizeof(double)));
   SK_CUDA(c.yinc.ensure(npairs * ly * ld * sizeof(double)));
-  SK_CUDA(launch_increments(d_xraw, npairs, lx, dim, ld, c.xinc.as<double>(), c.stream()));
-  SK_CUDA(launch_increments(d_yraw, npairs, ly, dim, ld, c.yinc.as<double>(), c.stream()));
-  c.aux_launches += 2;
+  // with the adaptive policy the per-series max squared increment norms come
+  // out of the same pass (the order proof below)
+  if (adaptive) SK_CUDA(c.sqn.ensure(2 * npairs * sizeof(double)));
+  SK_CUDA(launch_increments(d_xraw, npairs, lx, dim, ld, c.xinc.as<double>(), c.stream(),
+                            adaptive ? c.sqn.as<double>() : nullptr));
+  SK_CUDA(launch_increments(d_yraw, npairs, ly, dim, ld, c.yinc.as<double>(), c.stream(),
+                            adaptive ? c.sqn.as<double>() + npairs : nullptr));
+  c.aux_launches += adaptive && ld > 16 ? 4 : 2;
   PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), lx * ld, ly * ld, static_cast<int>(cy),
              static_cast<int>(cx), static_cast<int>(dim), static_cast<int>(ld)};
   std::vector<uint32_t> px(npairs), py(npairs), pout(npairs);
   for (size_t k = 0; k < npairs; ++k) px[k] = py[k] = pout[k] = static_cast<uint32_t>(k);
   if (adaptive) {
-    SK_CUDA(c.sqn.ensure(2 * npairs * sizeof(double)));
-    SK_CUDA(launch_max_sqnorm(ps.d_xinc, npairs, cx, dim, ld, c.sqn.as<double>(), c.stream()));
-    SK_CUDA(launch_max_sqnorm(ps.d_yinc, npairs, cy, dim, ld, c.sqn.as<double>() + npairs, c.stream()));
-    c.aux_launches += 2;
     std::vector<double> h(2 * npairs);
     SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, 2 * npairs * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
     SK_CUDA(cudaStreamSynchronize(c.stream()));
@@ -1080,16 +1081,15 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
   SK_CUDA(c.xinc.ensure(m * len * ld * sizeof(double)));
   SK_CUDA(c.values.ensure(np * sizeof(double)));
   SK_CUDA(cudaMemcpyAsync(c.raw_x.p, family, m * len * dim * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
-  SK_CUDA(launch_increments(c.raw_x.as<double>(), m, len, dim, ld, c.xinc.as<double>(), c.stream()));
-  ++c.aux_launches;
+  if (adaptive) SK_CUDA(c.sqn.ensure(m * sizeof(double)));
+  SK_CUDA(launch_increments(c.raw_x.as<double>(), m, len, dim, ld, c.xinc.as<double>(), c.stream(),
+                            adaptive ? c.sqn.as<double>() : nullptr));
+  c.aux_launches += adaptive && ld > 16 ? 2 : 1;
   // propagate(padded[i], padded[j]): x = member i (columns), y = member j (rows)
   PairSet ps{c.xinc.as<double>(), c.xinc.as<double>(), len * ld, len * ld, static_cast<int>(cnt),
              static_cast<int>(cnt), static_cast<int>(dim), static_cast<int>(ld)};
   std::vector<int> ords, conv;
   if (adaptive) {
-    SK_CUDA(c.sqn.ensure(m * sizeof(double)));
-    SK_CUDA(launch_max_sqnorm(ps.d_xinc, m, cnt, dim, ld, c.sqn.as<double>(), c.stream()));
-    ++c.aux_launches;
     std::vector<double> h(m);
     SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, m * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
     SK_CUDA(cudaStreamSynchronize(c.stream()));

@@ -28,8 +28,11 @@ inline size_t inc_ld(size_t dim) {
   const int dp = pick_dp(dim);
   return dp > 0 ? static_cast<size_t>(dp) : (dim + 3) / 4 * 4;
 }
+// Increments rows (zero row first, ld doubles per row); with sqn (device,
+// nseries doubles) also each series' max squared increment norm, fused for
+// ld <= 16.
 cudaError_t launch_increments(const double* v, size_t nseries, size_t len, size_t dim, size_t ld, double* out,
-                              cudaStream_t st);
+                              cudaStream_t st, double* sqn = nullptr);
 cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, size_t dim, size_t ld, double* out,
                               cudaStream_t st);
 cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
