@@ -122,18 +122,14 @@ int host_estimate_order(double rho, double tol, int* order, int* converged) {
 // wavefront.cpp:19-30,107,111-125,175-176 -- the 1-thread live-series
 // counter in closed form: the count only rises in prefill_units, and inside a
 // diagonal every tile does sub(2) then add(up + right <= 2), so the peak is
-// reached right after a prefill.  O(rows + cols).
+// reached right after a prefill.  With m = min(rows, cols): diagonals
+// 0..m-2 each prefill both edges (+2, nothing retires yet), reaching 2m; if
+// the longer edge keeps going, diagonal m-1 prefills it once more (+1) before
+// the shorter edge's retirements balance each later prefill.  Checked
+// against the diagonal-by-diagonal count in tests/test_host.py.
 uint64_t peak_live_closed_form(uint64_t rows, uint64_t cols) {
-  int64_t cur = 2, peak = 2;  // prefill_units(0): both edges live
-  const uint64_t diagonals = rows + cols - 1;
-  for (uint64_t d = 0; d < diagonals; ++d) {
-    if (d + 1 < diagonals) {
-      cur += (d + 1 <= cols - 1 ? 1 : 0) + (d + 1 <= rows - 1 ? 1 : 0);
-      if (cur > peak) peak = cur;
-    }
-    cur -= (d >= rows - 1 ? 1 : 0) + (d >= cols - 1 ? 1 : 0);
-  }
-  return static_cast<uint64_t>(peak);
+  const uint64_t m = std::min(rows, cols), big = std::max(rows, cols);
+  return 2 * m + (big > m ? 1 : 0);
 }
 
 // ----------------------------------------------------------------- context
@@ -1064,14 +1060,18 @@ int sk_pairwise(const double* xs, size_t lx, const double* ys, size_t ly, size_t
   SK_CUDA(c.raw_x.ensure(npairs * lx * dim * sizeof(double)));
   SK_CUDA(c.raw_y.ensure(npairs * ly * dim * sizeof(double)));
   SK_CUDA(c.values.ensure(npairs * sizeof(double)));
+  Tracer tr;
   SK_CUDA(h2d(c, c.raw_x.p, xs, npairs * lx * dim * sizeof(double)));
   SK_CUDA(h2d(c, c.raw_y.p, ys, npairs * ly * dim * sizeof(double)));
+  tr.mark("pairwise: h2d issued");
   PairwiseResult res;
   if (int rc = pairwise_core(c, c.raw_x.as<double>(), lx, c.raw_y.as<double>(), ly, npairs, dim, adaptive, order,
                              tol, flags, c.values.as<double>(), adaptive && max_abs_rho, nullptr, nullptr, res, st))
     return rc;
+  tr.mark("pairwise: core");
   SK_CUDA(cudaMemcpy(values, c.values.p, npairs * sizeof(double), cudaMemcpyDeviceToHost));
   fill_pair_outputs(res, npairs, values, orders, converged, max_abs_rho, per_pair, xs, lx, ys, ly, dim);
+  tr.mark("pairwise: outputs");
   return SK_OK;
 }
 

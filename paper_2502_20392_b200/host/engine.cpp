@@ -44,18 +44,11 @@ uint32_t flags_of(const PropagateOptions& o) {
   return (o.strict_corner ? SK_STRICT_CORNER : 0u) | (tile::detail::w_fault_for_testing() ? SK_W_FAULT : 0u);
 }
 
-// wavefront.cpp live-series counter, closed form (see sk_capi.cu)
+// wavefront.cpp live-series counter, closed form (derivation in sk_capi.cu
+// peak_live_closed_form)
 std::size_t peak_live(std::size_t rows, std::size_t cols) {
-  long cur = 2, peak = 2;
-  const std::size_t diagonals = rows + cols - 1;
-  for (std::size_t d = 0; d < diagonals; ++d) {
-    if (d + 1 < diagonals) {
-      cur += (d + 1 <= cols - 1 ? 1 : 0) + (d + 1 <= rows - 1 ? 1 : 0);
-      peak = std::max(peak, cur);
-    }
-    cur -= (d >= rows - 1 ? 1 : 0) + (d >= cols - 1 ? 1 : 0);
-  }
-  return static_cast<std::size_t>(peak);
+  const std::size_t m = std::min(rows, cols), big = std::max(rows, cols);
+  return 2 * m + (big > m ? 1 : 0);
 }
 
 KernelResult run(const TimeSeries& x, const TimeSeries& y, int order, const PropagateOptions& options, bool grid) {

@@ -482,15 +482,11 @@ class GramResult:
 
 
 def _peak_live(rows: int, cols: int) -> int:
-    # wavefront.cpp live counter, closed form (same as the C-ABI's)
-    cur = peak = 2
-    diagonals = rows + cols - 1
-    for d in range(diagonals):
-        if d + 1 < diagonals:
-            cur += (1 if d + 1 <= cols - 1 else 0) + (1 if d + 1 <= rows - 1 else 0)
-            peak = max(peak, cur)
-        cur -= (1 if d >= rows - 1 else 0) + (1 if d >= cols - 1 else 0)
-    return peak
+    # wavefront.cpp live counter in closed form (same as the C-ABI's
+    # peak_live_closed_form): 2 per diagonal while both edges prefill, one
+    # more when the longer edge keeps prefilling past the shorter one
+    m, big = min(rows, cols), max(rows, cols)
+    return 2 * m + (1 if big > m else 0)
 
 
 def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: int = 0,

@@ -83,6 +83,13 @@ def test_peak_live_closed_form(restatement, rows, cols):
     assert sk._peak_live(rows, cols) == restatement.peak_live(rows, cols)
 
 
+def test_peak_live_closed_form_dense(restatement):
+    from paper_2502_20392_b200 import sigker as sk
+    for rows in range(1, 48):
+        for cols in range(1, 48):
+            assert sk._peak_live(rows, cols) == restatement.peak_live(rows, cols), (rows, cols)
+
+
 def test_time_series_contract():
     from paper_2502_20392_b200 import sigker as sk
     with pytest.raises(ValueError):
