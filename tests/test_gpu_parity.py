@@ -325,6 +325,26 @@ def test_large_dim_table_path(sk, restatement):
         assert sk.IncrementTable(x, y).max_abs_rho() == restatement.max_abs_rho(x, y)
 
 
+def test_cfg4_shape_dmma_table_path(sk, restatement):
+    """BASELINE config 4's shape (d = 512, the DMMA rho-table path) at a
+    length the oracle finishes in seconds: adaptive single pair and a ragged
+    batch, against the restatement (same orders; 1e-10 at N <= 16, bit-exact
+    on the literal kernel above)."""
+    x = restatement.brownian(257, 512, 41)
+    y = restatement.brownian(193, 512, 42)
+    v_ref, n_ref, _ = restatement.propagate_with_policy(x, y, 1e-12, check_corner=False)
+    r = sk.propagate_with_policy(x, y, sk.TruncationPolicy.adaptive(1e-12), sk.PropagateOptions(strict_corner=False))
+    assert r.order == n_ref
+    assert (r.value == v_ref) if n_ref > 16 else rel(r.value, v_ref) < TOL
+    xs = np.stack([restatement.brownian(130, 512, 50 + k) for k in range(3)])
+    ys = np.stack([restatement.brownian(97, 512, 60 + k) for k in range(3)])
+    res = sk.pairwise(xs, ys, sk.TruncationPolicy.fixed(8), sk.PropagateOptions(strict_corner=False))
+    assert not res.failures
+    for k in range(3):
+        v, _ = restatement.propagate(xs[k], ys[k], 8, check_corner=False)
+        assert rel(res.values[k], v) < TOL, k
+
+
 def test_max_abs_rho_bit_exact(sk, restatement):
     rng = restatement.rng(99)
     for d in (1, 2, 3, 5, 8, 13, 16, 33):
