@@ -489,6 +489,16 @@ def _peak_live(rows: int, cols: int) -> int:
     return 2 * m + (1 if big > m else 0)
 
 
+def _status_array(n: int) -> np.ndarray:
+    """n zeroed sk_status records as a numpy structured array (calloc'd pages,
+    vectorised code scans) with the C layout of include/sigker_b200.h."""
+    S = _capi.SkStatus
+    dt = np.dtype({"names": ["code", "tile_k", "tile_l", "message"], "formats": ["<i4", "<u8", "<u8", "S256"],
+                   "offsets": [S.code.offset, S.tile_k.offset, S.tile_l.offset, S.message.offset],
+                   "itemsize": ctypes.sizeof(S)})
+    return np.zeros(n, dtype=dt)
+
+
 def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: int = 0,
                 nshards: int = 1) -> GramResult:
     """gram.hpp:46 (gram.cpp:16-98).  With nshards > 1 only this shard's
@@ -517,7 +527,7 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     pmax = np.zeros(m * m)
     maxp = ctypes.c_double()
     conv = ctypes.c_int()
-    per = (_capi.SkStatus * (m * m))()
+    per = _status_array(m * m)
     flags = _capi.SK_STRICT_CORNER if options.strict_corner else 0
     if _W_FAULT[0]:
         flags |= _capi.SK_W_FAULT
@@ -526,7 +536,8 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     def run_shard(sub, nsub, vals, ords, pm, mp, cv, pr, status):
         return lib.sk_gram(_ptr(padded), m, max_len, dim, 1 if adaptive else 0, int(options.policy.order),
                            float(options.policy.tol), flags, 1 if scan else 0, int(sub), int(nsub), _ptr(vals),
-                           _ptr(ords), _ptr(pm), ctypes.byref(mp), ctypes.byref(cv), pr, ctypes.byref(status))
+                           _ptr(ords), _ptr(pm), ctypes.byref(mp), ctypes.byref(cv), _ptr(pr),
+                           ctypes.byref(status))
 
     devices = list(options.devices)
     if len(devices) <= 1:
@@ -540,7 +551,7 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
         import threading
         nd = len(devices)
         parts = [dict(values=np.zeros(m * m), orders=np.zeros(m * m, dtype=np.int32), pmax=np.zeros(m * m),
-                      maxp=ctypes.c_double(), conv=ctypes.c_int(), per=(_capi.SkStatus * (m * m))(),
+                      maxp=ctypes.c_double(), conv=ctypes.c_int(), per=_status_array(m * m),
                       st=_capi.SkStatus(), rc=0) for _ in range(nd)]
 
         def work(k):
@@ -559,29 +570,29 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
             _check(p["rc"], p["st"])
         lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
         owner = np.full(m * m, -1)
-        tri = [(i, j) for i in range(m) for j in range(i, m)]
+        iu, ju = np.triu_indices(m)  # the upper triangle in row-major order, as the shards number it
         for k in range(nd):
             lib.sk_gram_shard_range(m, shard * nd + k, nshards * nd, ctypes.byref(lo), ctypes.byref(hi))
-            for (i, j) in tri[lo.value:hi.value]:
-                owner[i * m + j] = owner[j * m + i] = k
+            a, b = iu[lo.value:hi.value], ju[lo.value:hi.value]
+            owner[a * m + b] = k
+            owner[b * m + a] = k
         values[:] = np.nan
         for k, p in enumerate(parts):
             sel = owner == k
             values[sel] = p["values"][sel]
             orders[sel] = p["orders"][sel]
             pmax[sel] = p["pmax"][sel]
-            for e in np.nonzero(sel)[0]:
-                per[e] = p["per"][e]
+            per[sel] = p["per"][sel]
         maxp.value = max(p["maxp"].value for p in parts)
         conv.value = int(all(p["conv"].value for p in parts))
     wall = time.perf_counter() - t0
     r = GramResult(size=m, values=values, orders=orders, adaptive=adaptive, orders_converged=bool(conv.value),
                    wall_seconds=wall)
-    for i in range(m):
-        for j in range(i, m):
-            e = per[i * m + j]
-            if e.code != 0:
-                r.failures.append(GramEntryError(i, j, e.message.decode(errors="replace")))
+    # failing upper-triangle entries in (i, j) row-major order
+    for e in np.flatnonzero(per["code"] != 0):
+        i, j = divmod(int(e), m)
+        if j >= i:
+            r.failures.append(GramEntryError(i, j, per["message"][e].decode(errors="replace")))
     computed = orders[orders > 0]
     r.min_order = int(computed.min()) if computed.size else 0
     r.max_order = int(computed.max()) if computed.size else 0
