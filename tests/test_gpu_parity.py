@@ -455,6 +455,25 @@ def test_gram_over_a_device_list_matches_one_call(sk, restatement):
     assert two.orders_converged == one.orders_converged
 
 
+def test_gram_device_list_merges_entry_failures(sk, restatement):
+    """Entries that overflow (NumericOverflowError -> NaN + a failures record,
+    gram.cpp:74-77) merge from the device-list sub-shards exactly as one call
+    reports them: same NaN cells, same (i, j, message) records in order."""
+    rng = restatement.rng(405)
+    fam = [rng.random_series(30 + 2 * k, 1, 1.0) for k in range(7)]
+    fam[4] = fam[4] * 3e3  # |delta| > 1.25e5 against itself and the larger series
+    pol = sk.TruncationPolicy.fixed(8)
+    one = sk.gram_matrix(fam, sk.GramOptions(policy=pol, strict_corner=False))
+    two = sk.gram_matrix(fam, sk.GramOptions(policy=pol, strict_corner=False, devices=[0, 0]))
+    assert one.failures, "the scaled series must overflow somewhere"
+    assert [(f.row, f.col, f.message) for f in two.failures] == [(f.row, f.col, f.message) for f in one.failures]
+    assert all(f.row <= f.col for f in one.failures)
+    assert (4, 4) in [(f.row, f.col) for f in one.failures]
+    assert np.isnan(np.asarray(two.values)).tolist() == np.isnan(np.asarray(one.values)).tolist()
+    for f in one.failures:
+        assert "rescale" in f.message
+
+
 def test_baseline_size_batch_properties(sk, restatement):
     """BASELINE config 2 at full size (256 pairs, l = 4096, d = 8, adaptive)
     through the throughput schedule: four pairs against the restatement, and
