@@ -428,18 +428,18 @@ def pairwise(xs, ys, policy: Optional[TruncationPolicy] = None, options: Optiona
     orders = np.zeros(npairs, dtype=np.int32)
     conv = np.zeros(npairs, dtype=np.int32)
     mr = np.zeros(npairs) if want_max_abs_rho else None
-    per = (_capi.SkStatus * max(npairs, 1))()
+    per = _status_array(max(npairs, 1))
     adaptive = 1 if policy.mode == "adaptive" else 0
     rc = lib.sk_pairwise(_ptr(xs), lx, _ptr(ys), ly, npairs, d, adaptive, int(policy.order), float(policy.tol),
                          _flags(options), _ptr(values), _ptr(orders), _ptr(conv),
-                         _ptr(mr) if mr is not None else None, per, ctypes.byref(st))
+                         _ptr(mr) if mr is not None else None, _ptr(per), ctypes.byref(st))
     _check(rc, st)
     failures = []
-    for k in range(npairs):
-        if per[k].code == _capi.SK_INCONSISTENT_BOUNDARY:
-            _raise(per[k])
-        if per[k].code != 0:
-            failures.append((k, int(per[k].tile_k), int(per[k].tile_l), per[k].message.decode(errors="replace")))
+    for k in np.flatnonzero(per["code"][:npairs] != 0).tolist():
+        e = per[k]
+        if e["code"] == _capi.SK_INCONSISTENT_BOUNDARY:
+            _raise(_capi.SkStatus.from_buffer_copy(e.tobytes()))
+        failures.append((k, int(e["tile_k"]), int(e["tile_l"]), e["message"].decode(errors="replace")))
     return PairwiseResult(values, orders, conv.astype(bool), mr, failures)
 
 
