@@ -41,3 +41,6 @@ TimeSeries near_periodic(std::size_t length, std::size_t dim, double period, dou
                          std::uint64_t seed);
 
 }  // namespace sigker::datagen
+
+// C binding of brownian() (row-major length x dim into `out`; 0 on success).
+extern "C" int sigker_datagen_brownian(std::size_t length, std::size_t dim, std::uint64_t seed, double* out);

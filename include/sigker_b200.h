@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SK_ABI_VERSION 2
+#define SK_ABI_VERSION 3
 
 /* Status codes (errors.hpp:10-53 of the reference). */
 enum sk_code {
@@ -118,14 +118,33 @@ int sk_pairwise_device(const double* d_xs, size_t lx, const double* d_ys, size_t
  * writes mirrored entries of values/orders (m*m; untouched entries are NaN /
  * 0).  scan_products != 0 (adaptive or compute_bound): pair_max (m*m, may be
  * NULL) receives each pair's exact max|rho| and *max_product their maximum.
- * entry_status (m*m, may be NULL) receives per-entry NumericOverflowError
- * records; any other per-entry failure (InconsistentBoundaryError) is
- * returned as the call's status, as gram.cpp:74-77 only catches overflow.
+ * Entries that raise NumericOverflowError are NaN and counted in
+ * *n_failures; their records come from sk_gram_failures.  Any other
+ * per-entry failure (InconsistentBoundaryError) is returned as the call's
+ * status, as gram.cpp:74-77 only catches overflow.
  * converged <- 0 if any adaptive search saturated. */
 int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
             uint32_t flags, int scan_products, size_t shard, size_t nshards, double* values, int* orders,
-            double* pair_max, double* max_product, int* converged, sk_status* entry_status,
-            sk_status* st);
+            double* pair_max, double* max_product, int* converged, size_t* n_failures, sk_status* st);
+
+/* The same on a device-resident family (d_family: m*len*dim doubles in this
+ * thread's device memory) for the upper-triangle pair range [first, last)
+ * (row-major, 0 <= first <= last <= m(m+1)/2): each pair's value -- NaN for
+ * an overflow entry -- goes into both mirrored cells of the device matrix
+ * d_matrix (m*m doubles); other cells are not touched.  Work is issued on
+ * the thread's stream (sk_set_stream); the call returns when it is done. */
+int sk_gram_device(const double* d_family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
+                   uint32_t flags, int scan_products, size_t first, size_t last, double* d_matrix,
+                   double* max_product, int* converged, size_t* n_failures, sk_status* st);
+
+/* One overflow entry of the calling thread's last sk_gram / sk_gram_device
+ * call (gram.hpp:20-24 GramEntryError).  sk_gram_failures copies up to cap
+ * records in (row, col) row-major order and returns how many it copied. */
+typedef struct sk_gram_failure {
+  uint32_t row, col; /* row <= col */
+  sk_status status;
+} sk_gram_failure;
+size_t sk_gram_failures(sk_gram_failure* out, size_t cap);
 
 /* Row-major upper-triangle pair indices [first, last) that shard `shard` of
  * `nshards` evaluates in sk_gram (equal pair counts; pairs cost the same
@@ -174,7 +193,7 @@ typedef struct sk_stats {
   double tile_flops;       /* algorithmic FP64 flops, sum of F(N,d) per tile */
   uint64_t table_launches; /* rho-table builds (d > 16: DMMA GEMM)        */
   double table_ms;         /* summed device time of those builds          */
-  uint64_t paired_launches; /* sweep launches with two-warp (paired) bands (ABI 2) */
+  uint64_t literal_rechecks; /* strict corner: pairs re-swept with the literal kernel (ABI 3) */
 } sk_stats;
 
 int sk_stats_enable(int enable);

@@ -79,6 +79,8 @@ class Restatement:
         L.or_gram_error_bound.restype = ctypes.c_double
         L.or_gram_error_bound.argtypes = [SZ, SZ, ctypes.c_double, ctypes.c_int]
         L.or_gram.argtypes = [P, SZ, SZ, SZ, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, P, P, P, P]
+        L.or_propagate_probe.argtypes = [P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_int, P, SZ, P, P, P, P, P,
+                                         ctypes.POINTER(Status)]
         self.L = L
 
     # datagen
@@ -133,6 +135,24 @@ class Restatement:
                                  ctypes.byref(v), ctypes.byref(pk), _ptr(g) if grid else None, ctypes.byref(st))
         _raise(rc, st)
         return (v.value, int(pk.value), g) if grid else (v.value, int(pk.value))
+
+    def propagate_probe(self, x, y, order, knots=(), check_corner=False):
+        """The same sweep with instrumentation: K at the knots (a, a), the worst
+        relative corner mismatch, and the first tile (k, l) where the
+        reference's corner check (tile_series.cpp:70-75) would throw (0, 0 if
+        none).  Returns (value, knot_values, max_corner_rel, (k, l))."""
+        x, y = np.ascontiguousarray(x, float), np.ascontiguousarray(y, float)
+        kn = np.ascontiguousarray(knots, dtype=np.uint64)
+        kv = np.full(len(kn), np.nan)
+        v, mc = ctypes.c_double(), ctypes.c_double()
+        ck, cl = ctypes.c_uint64(), ctypes.c_uint64()
+        st = Status()
+        rc = self.L.or_propagate_probe(_ptr(x), x.shape[0], _ptr(y), y.shape[0], x.shape[1], order,
+                                       1 if check_corner else 0, _ptr(kn) if len(kn) else None, len(kn),
+                                       _ptr(kv) if len(kn) else None, ctypes.byref(mc), ctypes.byref(ck),
+                                       ctypes.byref(cl), ctypes.byref(v), ctypes.byref(st))
+        _raise(rc, st)
+        return v.value, kv, mc.value, (int(ck.value), int(cl.value))
 
     def propagate_with_policy(self, x, y, tol, check_corner=True):
         n, conv = self.estimate_order(self.max_abs_rho(x, y), tol)

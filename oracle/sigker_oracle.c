@@ -325,9 +325,45 @@ uint64_t or_peak_live(size_t rows, size_t cols) {
  * series are kept per column (alpha) and per row (beta) instead of the
  * reference's diagonal slots; tiles on one diagonal touch disjoint entries,
  * so the arithmetic and its order per tile are unchanged. */
+/* Instrumentation of the same sweep (results are unchanged by it):
+ *   knots/knot_vals: K at grid points (a, a) for each a in knots (the total of
+ *     tile (a-1, a-1)); entries beyond the grid are left untouched;
+ *   corner: worst |alpha0-beta0| / max(1,|alpha0|,|beta0|) over all tiles, and
+ *     the first tile (diagonal order, 1-based k along x) where it exceeds 1e-9
+ *     -- the tile at which the reference would throw (tile_series.cpp:70-75). */
+typedef struct {
+  const size_t* knots;
+  size_t nknots;
+  double* knot_vals;
+  double max_corner_rel;
+  uint64_t corner_k, corner_l;
+} or_probe;
+
+static int propagate_core(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
+                          int check_corner, double* value, uint64_t* peak_live, double* grid_or_null,
+                          or_status* st, or_probe* pr);
+
 int or_propagate(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
                  int check_corner, double* value, uint64_t* peak_live, double* grid_or_null,
                  or_status* st) {
+  return propagate_core(x, lx, y, ly, dim, order, check_corner, value, peak_live, grid_or_null, st, NULL);
+}
+
+int or_propagate_probe(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
+                       int check_corner, const size_t* knots, size_t nknots, double* knot_vals,
+                       double* max_corner_rel, uint64_t* corner_k, uint64_t* corner_l, double* value,
+                       or_status* st) {
+  or_probe pr = {knots, nknots, knot_vals, 0.0, 0, 0};
+  const int rc = propagate_core(x, lx, y, ly, dim, order, check_corner, value, NULL, NULL, st, &pr);
+  *max_corner_rel = pr.max_corner_rel;
+  *corner_k = pr.corner_k;
+  *corner_l = pr.corner_l;
+  return rc;
+}
+
+static int propagate_core(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
+                          int check_corner, double* value, uint64_t* peak_live, double* grid_or_null,
+                          or_status* st, or_probe* pr) {
   if (st) memset(st, 0, sizeof *st);
   if (lx < 2 || ly < 2) {
     st_set(st, OR_INVALID, 0, 0, "propagate: both series need length >= 2");
@@ -370,6 +406,17 @@ int or_propagate(const double* x, size_t lx, const double* y, size_t ly, size_t 
       }
       double* a = alpha + j * n;
       double* b = beta + i * n;
+      if (pr) {
+        double sc = 1.0;
+        if (fabs(a[0]) > sc) sc = fabs(a[0]);
+        if (fabs(b[0]) > sc) sc = fabs(b[0]);
+        const double rel = fabs(a[0] - b[0]) / sc;
+        if (rel > pr->max_corner_rel) pr->max_corner_rel = rel;
+        if (pr->corner_k == 0 && or_corner_mismatch(a[0], b[0])) {
+          pr->corner_k = j + 1;
+          pr->corner_l = i + 1;
+        }
+      }
       if (check_corner && or_corner_mismatch(a[0], b[0])) { /* tile_series.cpp:70-75 */
         st_set(st, OR_INCONSISTENT, j + 1, i + 1, "boundary series disagree at the shared corner");
         rc = OR_INCONSISTENT;
@@ -385,6 +432,9 @@ int or_propagate(const double* x, size_t lx, const double* y, size_t ly, size_t 
       memcpy(b, out_b, n * sizeof(double));
       if (grid_or_null) grid_or_null[(j + 1) * ly + (i + 1)] = total;
       if (i + 1 == rows && j + 1 == cols) final_value = total;
+      if (pr && i == j)
+        for (size_t q = 0; q < pr->nknots; ++q)
+          if (pr->knots[q] == i + 1) pr->knot_vals[q] = total;
     }
   }
   if (rc == OR_OK) {

@@ -27,7 +27,8 @@ SK_W_FAULT = 4
 EXPORTED = [
     "sk_abi_version", "sk_device_count", "sk_set_device", "sk_set_stream",
     "sk_propagate", "sk_max_abs_rho", "sk_estimate_order", "sk_step_tile",
-    "sk_step_tile_fast", "sk_pairwise", "sk_pairwise_device", "sk_gram", "sk_gram_shard_range", "sk_all_finite",
+    "sk_step_tile_fast", "sk_pairwise", "sk_pairwise_device", "sk_gram", "sk_gram_device", "sk_gram_failures",
+    "sk_gram_shard_range", "sk_all_finite",
     "sk_stats_enable", "sk_stats_reset", "sk_stats_get", "sk_release",
     "sk_strip_bands", "sk_exchange_alloc", "sk_exchange_reset", "sk_exchange_free", "sk_ipc_handle",
     "sk_ipc_open", "sk_ipc_close", "sk_enable_peer_access", "sk_propagate_strip", "sk_propagate_split",
@@ -39,11 +40,15 @@ class SkStatus(ctypes.Structure):
                 ("tile_l", ctypes.c_uint64), ("message", ctypes.c_char * 256)]
 
 
+class SkGramFailure(ctypes.Structure):
+    _fields_ = [("row", ctypes.c_uint32), ("col", ctypes.c_uint32), ("status", SkStatus)]
+
+
 class SkStats(ctypes.Structure):
     _fields_ = [("sweep_launches", ctypes.c_uint64), ("aux_launches", ctypes.c_uint64),
                 ("sweep_ms", ctypes.c_double), ("tiles", ctypes.c_double),
                 ("tile_flops", ctypes.c_double), ("table_launches", ctypes.c_uint64),
-                ("table_ms", ctypes.c_double), ("paired_launches", ctypes.c_uint64)]
+                ("table_ms", ctypes.c_double), ("literal_rechecks", ctypes.c_uint64)]
 
 
 _lib = None
@@ -81,6 +86,9 @@ def load():
                                 ctypes.c_uint32, P, P, P, P, ST], ctypes.c_int),
         "sk_gram": ([P, SZ, SZ, SZ, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint32, ctypes.c_int,
                      SZ, SZ, P, P, P, P, P, P, ST], ctypes.c_int),
+        "sk_gram_device": ([P, SZ, SZ, SZ, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint32,
+                            ctypes.c_int, SZ, SZ, P, P, P, P, ST], ctypes.c_int),
+        "sk_gram_failures": ([P, SZ], SZ),
         "sk_gram_shard_range": ([SZ, SZ, SZ, P, P], ctypes.c_int),
         "sk_all_finite": ([P, SZ], ctypes.c_int),
         "sk_stats_enable": ([ctypes.c_int], ctypes.c_int),

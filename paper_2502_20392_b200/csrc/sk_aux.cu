@@ -317,6 +317,36 @@ __global__ void step_tile_fast_kernel(double delta, const double* __restrict__ i
   out[2 * (kMaxOrder + 1)] = total;
 }
 
+// Re-sweep bookkeeping (recheck_failures): reset the listed output slots'
+// error keys, and gather (value bits, error key) of the listed slots into one
+// contiguous buffer [values | keys] for a single device-to-host copy.
+__global__ void reset_slots_kernel(const uint32_t* __restrict__ idx, size_t n, unsigned long long* __restrict__ err) {
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x)
+    err[idx[t]] = ~0ull;
+}
+__global__ void gather_slots_kernel(const uint32_t* __restrict__ idx, size_t n, const double* __restrict__ values,
+                                    const unsigned long long* __restrict__ err, unsigned long long* __restrict__ out) {
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    out[t] = static_cast<unsigned long long>(__double_as_longlong(values[idx[t]]));
+    out[n + t] = err[idx[t]];
+  }
+}
+
+// sk_gram_device: launch slot t (pair (pi[t], pj[t])) into both mirrored cells
+// of the m x m matrix; a failed entry (error key set) is NaN (gram.cpp:74-77)
+__global__ void scatter_gram_kernel(const uint32_t* __restrict__ pi, const uint32_t* __restrict__ pj, size_t n,
+                                    size_t m, const double* __restrict__ values,
+                                    const unsigned long long* __restrict__ err, double* __restrict__ mat) {
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double v = err[t] == ~0ull ? values[t] : __longlong_as_double(0x7ff8000000000000ll);
+    mat[static_cast<size_t>(pi[t]) * m + pj[t]] = v;
+    mat[static_cast<size_t>(pj[t]) * m + pi[t]] = v;
+  }
+}
+
 // ------------------------------------------------------------- launchers
 static int grid_for(size_t work, int threads) {
   size_t g = (work + threads - 1) / threads;
@@ -411,6 +441,26 @@ cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint3
   }
   const dim3 grid((cols + kGT - 1) / kGT, (rows + kGT - 1) / kGT, static_cast<unsigned>(npairs));
   rho_gemm_kernel<<<grid, 128, kGemmSmem, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, ld, tab, tab_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset_slots(const uint32_t* idx, size_t n, unsigned long long* err, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  reset_slots_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx, n, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_slots(const uint32_t* idx, size_t n, const double* values, const unsigned long long* err,
+                                unsigned long long* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  gather_slots_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx, n, values, err, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_gram(const uint32_t* pi, const uint32_t* pj, size_t n, size_t m, const double* values,
+                                const unsigned long long* err, double* mat, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  scatter_gram_kernel<<<grid_for(n, 256), 256, 0, st>>>(pi, pj, n, m, values, err, mat);
   return cudaGetLastError();
 }
 

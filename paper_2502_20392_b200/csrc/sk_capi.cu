@@ -177,15 +177,16 @@ struct Ctx {
   cudaStream_t user = nullptr;
   int sms = 148;
   DevBuf raw_x, raw_y, xinc, yinc, sqn, pairs, values, err, maxr, prog, queue, abuf, tab, grid, diag, w65, tile_io,
-      scan, wd, susp, dep, rq;
+      scan, wd, susp, dep, rq, redo, redo_out, gpairs;
   bool stats_on = false;
   std::vector<StatRec> stats;
+  std::vector<sk_gram_failure> failures;  // the last sk_gram / sk_gram_device call's entry failures
   // host-side caches: cudaMemGetInfo can take milliseconds (driver round
   // trip), occupancy queries are per kernel variant and never change
   size_t free_cache = 0;
   int free_age = 0;
   std::map<int, int> occupancy;
-  uint64_t sweep_launches = 0, aux_launches = 0, table_launches = 0, paired_launches = 0;
+  uint64_t sweep_launches = 0, aux_launches = 0, table_launches = 0, literal_rechecks = 0;
   double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0, done_table_ms = 0.0;
 
   // pinned staging for large pageable uploads (h2d): two buffers per worker
@@ -202,7 +203,7 @@ struct Ctx {
     }
     DevBuf* all[] = {&raw_x, &raw_y, &xinc, &yinc, &sqn, &pairs, &values, &err, &maxr,
                      &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan, &wd,
-                     &susp,  &dep,   &rq};
+                     &susp,  &dep,   &rq,   &redo, &redo_out, &gpairs};
     for (DevBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
   }
@@ -389,7 +390,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
                const Strip& strip = Strip{}) {
   const size_t npairs_all = px.size();
   if (npairs_all == 0) return SK_OK;
-  const int ntempl = order <= kMaxRegOrder ? order : 0;
+  const int ntempl = order <= kMaxRegOrder && !(flags & kFlagLiteral) ? order : 0;
   const int dp = pick_dp(ps.dim);
   const int na = ntempl > 0 ? ntempl + 1 : kMaxOrder + 1;
   const int np = (na + 1) & ~1;
@@ -403,7 +404,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   if (auto it = c.occupancy.find(okey); it != c.occupancy.end()) {
     bps = it->second;
   } else {
-    SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, false, &bps));
+    SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, &bps));
     c.occupancy[okey] = bps;
   }
   if (bps < 1) return set_status(st, SK_CUDA_ERROR, 0, 0, "sweep kernel cannot be resident (occupancy 0)");
@@ -491,34 +492,13 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / (static_cast<size_t>(bands) * spb)));
   }
 
-  // Paired bands (sweep_pair_kernel, SK_PAIRED=1): every band of a streaming
-  // launch on two warps, alpha' and beta' split between them (the same bits).
-  // Opt-in: with tile totals formed only where a final tile can fall
-  // (kFlagAllTotals) the one-warp band has the shorter step (measured at
-  // l = 1001 / 4097: 552 ns one-warp vs 596 ns paired per wavefront step).
-  int pair_bps = 0;
-  bool paired = false;
-  const char* pe = std::getenv("SK_PAIRED");
-  if (pe && pe[0] == '1' && seg_cols == 0 && whole && !exact && ntempl > 0 && rows_per_lane(ntempl) == 1) {
-    const int pkey = okey | (1 << 30);
-    if (auto it = c.occupancy.find(pkey); it != c.occupancy.end()) {
-      pair_bps = it->second;
-    } else {
-      SK_CUDA(sweep_occupancy(ntempl, dp, false, extras, true, &pair_bps));
-      c.occupancy[pkey] = pair_bps;
-    }
-    paired = pair_bps > 0;
-  }
-
   for (size_t c0 = 0; c0 < npairs_all; c0 += chunk) {
     const size_t npairs = std::min(chunk, npairs_all - c0);
     const int nb = (strip.band_end < 0 ? bands : strip.band_end) - strip.band_begin;
     const unsigned long long units = static_cast<unsigned long long>(npairs) * nb;
-    const int bps_here = paired ? pair_bps : bps;
-    int blocks = bps_here * c.sms;
-    if (const char* e = std::getenv("SK_FORCE_BPS")) blocks = std::max(1, std::min(bps_here, std::atoi(e))) * c.sms;
-    // band workers: one-warp CTAs, or two-warp CTAs (paired)
-    const int per_block = paired ? 1 : kSweepWarps;
+    int blocks = bps * c.sms;
+    if (const char* e = std::getenv("SK_FORCE_BPS")) blocks = std::max(1, std::min(bps, std::atoi(e))) * c.sms;
+    const int per_block = kSweepWarps;
     const unsigned long long need_blocks = (units + per_block - 1) / per_block;
     if (static_cast<unsigned long long>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
     const size_t warps = static_cast<size_t>(blocks) * per_block;
@@ -644,10 +624,9 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     rec.tiles = static_cast<double>(npairs) * rows * cols;
     rec.flops = rec.tiles * flops_per_tile(order, ps.dim);
     if (int rc = record_start(c, &rec, st)) return rc;
-    SK_CUDA(sweep_launch(ntempl, dp, exact, extras, paired, blocks, c.stream(), P));
+    SK_CUDA(sweep_launch(ntempl, dp, exact, extras, blocks, c.stream(), P));
     if (int rc = record_end(c, &rec, st)) return rc;
     ++c.sweep_launches;
-    if (paired) ++c.paired_launches;
     if (int rc = check_watchdog(c, st)) return rc;
   }
   return SK_OK;
@@ -702,24 +681,18 @@ int adaptive_orders(Ctx& c, const PairSet& ps, const std::vector<double>& h_sqn_
   return SK_OK;
 }
 
-// decode an error key into the reference's exception contract
-int decode_err(unsigned long long key, sk_status* st, const double* xinc_host, const double* yinc_host,
-               size_t dim) {
+// decode an error key into the reference's exception contract; `delta` is the
+// failing tile's increment product for the overflow message (NaN if unknown)
+int decode_err(unsigned long long key, sk_status* st, double delta) {
   const unsigned code = static_cast<unsigned>(key & 3ull);
   const uint64_t i = (key >> 2) & 0x3fffffffull;
   const uint64_t d = key >> 32;
   const uint64_t j = d - i;
-  if (code == kErrDelta) {
-    double delta = std::numeric_limits<double>::quiet_NaN();
-    if (xinc_host && yinc_host) {
-      delta = 0.0;
-      for (size_t c = 0; c < dim; ++c) delta += xinc_host[j * dim + c] * yinc_host[i * dim + c];
-    }
+  if (code == kErrDelta)
     return set_status(st, SK_NUMERIC_OVERFLOW, j + 1, i + 1,
                       "increment product %f on tile (%llu, %llu) exceeds double range at any order; rescale "
                       "the inputs",
                       delta, static_cast<unsigned long long>(j + 1), static_cast<unsigned long long>(i + 1));
-  }
   if (code == kErrCorner)
     return set_status(st, SK_INCONSISTENT_BOUNDARY, j + 1, i + 1,
                       "boundary series disagree at the shared corner on tile (%llu, %llu)",
@@ -729,38 +702,94 @@ int decode_err(unsigned long long key, sk_status* st, const double* xinc_host, c
                     static_cast<unsigned long long>(j + 1), static_cast<unsigned long long>(i + 1));
 }
 
-// Throughput sweeps form tile totals only where a pair's final tile can fall
-// (kFlagAllTotals).  A pair that ended flagged (its first failure may be
-// preceded by an unchecked non-finite tile) or non-finite is swept again with
-// every total formed and checked: the reference's first failing tile, exactly.
-// Launch index t writes output slot t (values / err, hv / he on the host).
+// The failing tile's increment product for the overflow message
+// (wavefront.cpp:146-155): the two increment rows (device layout: row k + 1
+// holds dz_k, stride ld) come back and are dotted in the reference's order.
+// xs / ys: device increments of the pair's x and y series.  NaN unless `key`
+// is an increment-product overflow.
+double device_delta(Ctx& c, const double* xs, const double* ys, size_t ld, size_t dim, unsigned long long key) {
+  if ((key & 3ull) != kErrDelta) return std::numeric_limits<double>::quiet_NaN();
+  const uint64_t i = (key >> 2) & 0x3fffffffull;
+  const uint64_t j = (key >> 32) - i;
+  std::vector<double> a(ld), b(ld);
+  if (cudaMemcpyAsync(a.data(), xs + (j + 1) * ld, ld * sizeof(double), cudaMemcpyDeviceToHost, c.stream()) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(b.data(), ys + (i + 1) * ld, ld * sizeof(double), cudaMemcpyDeviceToHost, c.stream()) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(c.stream()) != cudaSuccess) {
+    cudaGetLastError();
+    return std::numeric_limits<double>::quiet_NaN();
+  }
+  double acc = 0.0;
+  for (size_t q = 0; q < dim; ++q) acc += a[q] * b[q];
+  return acc;
+}
+
+// Second sweeps after a throughput launch (launch index t writes output slot
+// t: values / err on the device, hv / he on the host).
+//  * Strict corner screen: a register-kernel pair whose first flagged tile is
+//    a corner screen (kCornerScreen, sk_device.cuh) is swept again with the
+//    literal kernel, which repeats the reference bit for bit -- so the
+//    reference's throw, its tile, or the value it returns, exactly.
+//  * Partial totals: throughput sweeps form tile totals only where a pair's
+//    final tile can fall (kFlagAllTotals).  A pair that ended flagged (its
+//    first failure may be preceded by an unchecked non-finite tile) or
+//    non-finite is swept again with every total formed and checked: the
+//    reference's first failing tile, exactly.  Not needed when the first
+//    sweep already formed every total (`all_totals`).
+// The flagged slots are reset by one scatter kernel, re-swept, and read back
+// with one gather (no per-pair API calls).
 int recheck_failures(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const std::vector<uint32_t>& py,
                      const std::vector<int>& ords, uint32_t flags, const Outputs& o, std::vector<double>& hv,
-                     std::vector<unsigned long long>& he, sk_status* st) {
-  std::vector<uint32_t> redo;
-  for (size_t t = 0; t < he.size(); ++t)
-    if (he[t] != ~0ull || !std::isfinite(hv[t])) redo.push_back(static_cast<uint32_t>(t));
-  if (redo.empty()) return SK_OK;
-  for (uint32_t t : redo) SK_CUDA(cudaMemsetAsync(o.d_err + t, 0xff, sizeof(unsigned long long), c.stream()));
-  std::vector<int> distinct;
-  for (uint32_t t : redo) distinct.push_back(ords[t]);
-  std::sort(distinct.begin(), distinct.end());
-  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
-  for (int ord : distinct) {
-    std::vector<uint32_t> gx, gy, go;
-    for (uint32_t t : redo)
-      if (ords[t] == ord) {
-        gx.push_back(px[t]);
-        gy.push_back(py[t]);
-        go.push_back(t);
-      }
-    if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags | kFlagAllTotals, o, st)) return rc;
+                     std::vector<unsigned long long>& he, bool all_totals, sk_status* st) {
+  std::vector<uint32_t> literal, totals;
+  for (size_t t = 0; t < he.size(); ++t) {
+    const bool corner = he[t] != ~0ull && (he[t] & 3ull) == kErrCorner;
+    if (corner && ords[t] <= kMaxRegOrder && (flags & kFlagStrictCorner))
+      literal.push_back(static_cast<uint32_t>(t));
+    else if (!all_totals && (he[t] != ~0ull || !std::isfinite(hv[t])))
+      totals.push_back(static_cast<uint32_t>(t));
   }
-  for (uint32_t t : redo) {
-    SK_CUDA(cudaMemcpyAsync(&hv[t], o.d_values + t, sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
-    SK_CUDA(cudaMemcpyAsync(&he[t], o.d_err + t, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream()));
+  if (literal.empty() && totals.empty()) return SK_OK;
+  for (int pass = 0; pass < 2; ++pass) {
+    const std::vector<uint32_t>& redo = pass == 0 ? literal : totals;
+    if (redo.empty()) continue;
+    const uint32_t extra = pass == 0 ? (kFlagLiteral | kFlagAllTotals) : kFlagAllTotals;
+    SK_CUDA(c.redo.ensure(redo.size() * sizeof(uint32_t)));
+    SK_CUDA(cudaMemcpyAsync(c.redo.p, redo.data(), redo.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                            c.stream()));
+    SK_CUDA(launch_reset_slots(c.redo.as<uint32_t>(), redo.size(), o.d_err, c.stream()));
+    ++c.aux_launches;
+    std::vector<int> distinct;
+    for (uint32_t t : redo) distinct.push_back(ords[t]);
+    std::sort(distinct.begin(), distinct.end());
+    distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+    for (int ord : distinct) {
+      std::vector<uint32_t> gx, gy, go;
+      for (uint32_t t : redo)
+        if (ords[t] == ord) {
+          gx.push_back(px[t]);
+          gy.push_back(py[t]);
+          go.push_back(t);
+        }
+      if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags | extra, o, st)) return rc;
+      if (pass == 0) c.literal_rechecks += gx.size();
+    }
+    // one gather of the re-swept slots' values and error keys
+    const size_t nr = redo.size();
+    SK_CUDA(c.redo_out.ensure(nr * 2 * sizeof(unsigned long long)));
+    SK_CUDA(launch_gather_slots(c.redo.as<uint32_t>(), nr, o.d_values, o.d_err,
+                                c.redo_out.as<unsigned long long>(), c.stream()));
+    ++c.aux_launches;
+    std::vector<unsigned long long> back(2 * nr);
+    SK_CUDA(cudaMemcpyAsync(back.data(), c.redo_out.p, back.size() * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c.stream()));
+    SK_CUDA(cudaStreamSynchronize(c.stream()));
+    for (size_t q = 0; q < nr; ++q) {
+      std::memcpy(&hv[redo[q]], &back[q], sizeof(double));
+      he[redo[q]] = back[nr + q];
+    }
   }
-  SK_CUDA(cudaStreamSynchronize(c.stream()));
   return SK_OK;
 }
 
@@ -841,17 +870,130 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
   SK_CUDA(cudaGetLastError());
   tr.mark("sweep done (sync)");
   // grid / diagonal sweeps form every total already
-  if (!d_grid && !d_diag)
-    if (int rc = recheck_failures(c, ps, px, py, res.orders, flags, o, hv, res.err, st)) return rc;
+  if (int rc = recheck_failures(c, ps, px, py, res.orders, flags, o, hv, res.err, d_grid || d_diag, st)) return rc;
   return SK_OK;
 }
 
-// host increments of one tile row/column pair for error messages
-std::vector<double> host_increments(const double* v, size_t len, size_t dim) {
-  std::vector<double> out((len - 1) * dim);
-  for (size_t k = 0; k + 1 < len; ++k)
-    for (size_t c = 0; c < dim; ++c) out[k * dim + c] = v[(k + 1) * dim + c] - v[k * dim + c];
-  return out;
+
+int gram_validate(size_t m, size_t len, size_t dim, int adaptive, int order, double tol, sk_status* st) {
+  if (m == 0) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: family must be nonempty");
+  if (dim < 1) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: dimension must be >= 1");
+  if (len < 2) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: common length must be >= 2");
+  if (adaptive ? !(tol > 0.0) : (order < 1 || order > kMaxOrder))
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, adaptive ? "adaptive tolerance must be positive"
+                                                             : "propagate: order must lie in [1, 64]");
+  return SK_OK;
+}
+
+// Gram core over device-resident raw series (family, m x len x dim): the
+// upper-triangle pairs [t0, t1) in row-major order (gram.cpp:39-42), as
+// gram.cpp:51-66 evaluates each entry -- increments, order (pre-pass proof or
+// exact scan), one sweep per distinct order, re-sweeps.  Leaves per-pair
+// results (launch slot t = pair t0 + t) on the host in `g` and the values /
+// error keys on the device (c.values, c.err); the failure records of the call
+// go to c.failures.
+struct GramCore {
+  std::vector<uint32_t> pi, pj;
+  std::vector<int> ords, conv;
+  std::vector<double> hv;
+  std::vector<unsigned long long> he, hm;
+};
+
+int gram_core(Ctx& c, const double* d_family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
+              uint32_t flags, bool want_max, size_t t0, size_t t1, GramCore& g, sk_status* st) {
+  c.failures.clear();
+  const size_t np = t1 - t0;
+  if (np == 0) return SK_OK;
+  // upper-triangle pairs (i <= j), row-major: locate t0, then walk
+  g.pi.resize(np);
+  g.pj.resize(np);
+  std::vector<uint32_t> pout(np);
+  {
+    size_t i = 0, row_start = 0;
+    while (i < m && row_start + (m - i) <= t0) {
+      row_start += m - i;
+      ++i;
+    }
+    size_t j = i + (t0 - row_start);
+    for (size_t t = 0; t < np; ++t) {
+      g.pi[t] = static_cast<uint32_t>(i);
+      g.pj[t] = static_cast<uint32_t>(j);
+      pout[t] = static_cast<uint32_t>(t);
+      if (++j == m) {
+        ++i;
+        j = i;
+      }
+    }
+  }
+  const size_t cnt = len - 1;
+  const size_t ld = inc_ld(dim);
+  SK_CUDA(c.xinc.ensure(m * len * ld * sizeof(double)));
+  SK_CUDA(c.values.ensure(np * sizeof(double)));
+  if (adaptive) SK_CUDA(c.sqn.ensure(m * sizeof(double)));
+  SK_CUDA(launch_increments(d_family, m, len, dim, ld, c.xinc.as<double>(), c.stream(),
+                            adaptive ? c.sqn.as<double>() : nullptr));
+  c.aux_launches += adaptive && ld > 16 ? 2 : 1;
+  // propagate(padded[i], padded[j]): x = member i (columns), y = member j (rows)
+  PairSet ps{c.xinc.as<double>(), c.xinc.as<double>(), len * ld, len * ld, static_cast<int>(cnt),
+             static_cast<int>(cnt), static_cast<int>(dim), static_cast<int>(ld)};
+  if (adaptive) {
+    std::vector<double> h(m);
+    SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, m * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    SK_CUDA(cudaStreamSynchronize(c.stream()));
+    if (int rc = adaptive_orders(c, ps, h, h, g.pi, g.pj, tol, g.ords, g.conv, st)) return rc;
+  } else {
+    g.ords.assign(np, order);
+    g.conv.assign(np, 1);
+  }
+  SK_CUDA(c.err.ensure(np * sizeof(unsigned long long)));
+  SK_CUDA(cudaMemsetAsync(c.err.p, 0xff, np * sizeof(unsigned long long), c.stream()));
+  SK_CUDA(cudaMemsetAsync(c.values.p, 0xff, np * sizeof(double), c.stream()));
+  if (want_max) {
+    SK_CUDA(c.maxr.ensure(np * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemsetAsync(c.maxr.p, 0, np * sizeof(unsigned long long), c.stream()));
+  }
+  Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(),
+            want_max ? c.maxr.as<unsigned long long>() : nullptr, nullptr, nullptr, 0, 0};
+  std::vector<int> distinct(g.ords.begin(), g.ords.end());
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  for (int ord : distinct) {
+    std::vector<uint32_t> gx, gy, go;
+    for (size_t k = 0; k < np; ++k)
+      if (g.ords[k] == ord) {
+        gx.push_back(g.pi[k]);
+        gy.push_back(g.pj[k]);
+        go.push_back(pout[k]);
+      }
+    if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags, o, st)) return rc;
+  }
+  g.hv.resize(np);
+  g.he.resize(np);
+  g.hm.assign(want_max ? np : 0, 0ull);
+  SK_CUDA(cudaMemcpyAsync(g.hv.data(), c.values.p, np * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(g.he.data(), c.err.p, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream()));
+  if (want_max)
+    SK_CUDA(cudaMemcpyAsync(g.hm.data(), c.maxr.p, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            c.stream()));
+  SK_CUDA(cudaStreamSynchronize(c.stream()));
+  SK_CUDA(cudaGetLastError());
+  if (int rc = recheck_failures(c, ps, g.pi, g.pj, g.ords, flags, o, g.hv, g.he, false, st)) return rc;
+  // gram.cpp:74-77: overflow entries become NaN + a failure record; anything
+  // else (the corner check) aborts the call with the first such entry's error
+  for (size_t t = 0; t < np; ++t) {
+    if (g.he[t] == ~0ull) continue;
+    if ((g.he[t] & 3ull) == kErrCorner) {
+      const unsigned long long key = g.he[t];
+      return decode_err(key, st, std::numeric_limits<double>::quiet_NaN());
+    }
+    sk_gram_failure f{};
+    f.row = g.pi[t];
+    f.col = g.pj[t];
+    decode_err(g.he[t], &f.status,
+               device_delta(c, ps.d_xinc + g.pi[t] * ps.sx, ps.d_xinc + g.pj[t] * ps.sx, ld, dim, g.he[t]));
+    c.failures.push_back(f);
+  }
+  return SK_OK;
 }
 
 }  // namespace
@@ -928,11 +1070,9 @@ int sk_propagate(const double* x, size_t lx, const double* y, size_t ly, size_t 
   if (int rc = pairwise_core(c, c.raw_x.as<double>(), lx, c.raw_y.as<double>(), ly, 1, dim, 0, order, 1e-12, flags,
                              c.values.as<double>(), false, d_grid, d_diag, res, st))
     return rc;
-  if (res.err[0] != ~0ull) {
-    const auto xi = host_increments(x, lx, dim);
-    const auto yi = host_increments(y, ly, dim);
-    return decode_err(res.err[0], st, xi.data(), yi.data(), dim);
-  }
+  if (res.err[0] != ~0ull)
+    return decode_err(res.err[0], st, device_delta(c, c.xinc.as<double>(), c.yinc.as<double>(), inc_ld(dim), dim,
+                                                   res.err[0]));
   SK_CUDA(cudaMemcpy(value, c.values.p, sizeof(double), cudaMemcpyDeviceToHost));
   if (grid) SK_CUDA(cudaMemcpy(grid, d_grid, lx * ly * sizeof(double), cudaMemcpyDeviceToHost));
   if (diag) SK_CUDA(cudaMemcpy(diag, d_diag, nd * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1025,23 +1165,20 @@ static int pairwise_validate(size_t lx, size_t ly, size_t dim, int adaptive, int
   return SK_OK;
 }
 
-static void fill_pair_outputs(const PairwiseResult& res, size_t npairs, double* values, int* orders,
-                              int* converged, double* max_abs_rho, sk_status* per_pair, const double* xs,
-                              size_t lx, const double* ys, size_t ly, size_t dim) {
+static void fill_pair_outputs(Ctx& c, const PairwiseResult& res, size_t npairs, double* values, int* orders,
+                              int* converged, double* max_abs_rho, sk_status* per_pair, size_t lx, size_t ly,
+                              size_t dim) {
+  const size_t ld = inc_ld(dim);
   for (size_t k = 0; k < npairs; ++k) {
     if (orders) orders[k] = res.orders[k];
     if (converged) converged[k] = res.conv[k];
     if (max_abs_rho && !res.maxr.empty()) std::memcpy(&max_abs_rho[k], &res.maxr[k], sizeof(double));
     if (res.err[k] != ~0ull) {
       if (values) values[k] = std::numeric_limits<double>::quiet_NaN();
-      if (per_pair) {
-        std::vector<double> xi, yi;
-        if (xs && ys) {
-          xi = host_increments(xs + k * lx * dim, lx, dim);
-          yi = host_increments(ys + k * ly * dim, ly, dim);
-        }
-        decode_err(res.err[k], &per_pair[k], xs ? xi.data() : nullptr, ys ? yi.data() : nullptr, dim);
-      }
+      if (per_pair)
+        decode_err(res.err[k], &per_pair[k],
+                   device_delta(c, c.xinc.as<double>() + k * lx * ld, c.yinc.as<double>() + k * ly * ld, ld, dim,
+                                res.err[k]));
     } else if (per_pair) {
       clear_status(&per_pair[k]);
     }
@@ -1066,11 +1203,11 @@ int sk_pairwise(const double* xs, size_t lx, const double* ys, size_t ly, size_t
   tr.mark("pairwise: h2d issued");
   PairwiseResult res;
   if (int rc = pairwise_core(c, c.raw_x.as<double>(), lx, c.raw_y.as<double>(), ly, npairs, dim, adaptive, order,
-                             tol, flags, c.values.as<double>(), adaptive && max_abs_rho, nullptr, nullptr, res, st))
+                             tol, flags, c.values.as<double>(), max_abs_rho != nullptr, nullptr, nullptr, res, st))
     return rc;
   tr.mark("pairwise: core");
   SK_CUDA(cudaMemcpy(values, c.values.p, npairs * sizeof(double), cudaMemcpyDeviceToHost));
-  fill_pair_outputs(res, npairs, values, orders, converged, max_abs_rho, per_pair, xs, lx, ys, ly, dim);
+  fill_pair_outputs(c, res, npairs, values, orders, converged, max_abs_rho, per_pair, lx, ly, dim);
   tr.mark("pairwise: outputs");
   return SK_OK;
 }
@@ -1087,151 +1224,108 @@ int sk_pairwise_device(const double* d_xs, size_t lx, const double* d_ys, size_t
   if (int rc = pairwise_core(*cp, d_xs, lx, d_ys, ly, npairs, dim, adaptive, order, tol, flags, d_values, false,
                              nullptr, nullptr, res, st))
     return rc;
-  fill_pair_outputs(res, npairs, nullptr, orders, converged, nullptr, per_pair, nullptr, lx, nullptr, ly, dim);
+  fill_pair_outputs(*cp, res, npairs, nullptr, orders, converged, nullptr, per_pair, lx, ly, dim);
   return SK_OK;
 }
 
 int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
             uint32_t flags, int scan_products, size_t shard, size_t nshards, double* values, int* orders,
-            double* pair_max, double* max_product, int* converged, sk_status* entry_status, sk_status* st) {
+            double* pair_max, double* max_product, int* converged, size_t* n_failures, sk_status* st) {
   clear_status(st);
-  if (m == 0) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: family must be nonempty");
-  if (dim < 1) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: dimension must be >= 1");
-  if (len < 2) return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: common length must be >= 2");
+  if (n_failures) *n_failures = 0;
+  if (int rc = gram_validate(m, len, dim, adaptive, order, tol, st)) return rc;
   if (nshards < 1 || shard >= nshards)
     return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: shard %zu out of range [0, %zu)", shard, nshards);
-  if (adaptive ? !(tol > 0.0) : (order < 1 || order > kMaxOrder))
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, adaptive ? "adaptive tolerance must be positive"
-                                                             : "propagate: order must lie in [1, 64]");
   Ctx* cp = nullptr;
   if (int rc = get_ctx(&cp, st)) return rc;
   Ctx& c = *cp;
+  c.failures.clear();
   size_t t0 = 0, t1 = 0;
   sk_gram_shard_range(m, shard, nshards, &t0, &t1);
-  const size_t np = t1 - t0;
   for (size_t k = 0; k < m * m; ++k) {
     if (values) values[k] = std::numeric_limits<double>::quiet_NaN();
     if (orders) orders[k] = 0;
     if (pair_max) pair_max[k] = 0.0;
-    if (entry_status) clear_status(&entry_status[k]);
   }
   if (max_product) *max_product = 0.0;
   if (converged) *converged = 1;
-  if (np == 0) return SK_OK;
-  // upper-triangle pairs (i <= j), row-major (gram.cpp:39-42)
-  std::vector<uint32_t> pi(np), pj(np), pout(np);
-  {
-    size_t t = 0, i = 0, j = 0;
-    // locate t0
-    size_t row_start = 0;
-    while (i < m && row_start + (m - i) <= t0) {
-      row_start += m - i;
-      ++i;
-    }
-    j = i + (t0 - row_start);
-    for (t = 0; t < np; ++t) {
-      pi[t] = static_cast<uint32_t>(i);
-      pj[t] = static_cast<uint32_t>(j);
-      pout[t] = static_cast<uint32_t>(t);
-      if (++j == m) {
-        ++i;
-        j = i;
-      }
-    }
-  }
-  const size_t cnt = len - 1;
-  const size_t ld = inc_ld(dim);
+  if (t1 == t0) return SK_OK;
   SK_CUDA(c.raw_x.ensure(m * len * dim * sizeof(double)));
-  SK_CUDA(c.xinc.ensure(m * len * ld * sizeof(double)));
-  SK_CUDA(c.values.ensure(np * sizeof(double)));
   SK_CUDA(h2d(c, c.raw_x.p, family, m * len * dim * sizeof(double)));
-  if (adaptive) SK_CUDA(c.sqn.ensure(m * sizeof(double)));
-  SK_CUDA(launch_increments(c.raw_x.as<double>(), m, len, dim, ld, c.xinc.as<double>(), c.stream(),
-                            adaptive ? c.sqn.as<double>() : nullptr));
-  c.aux_launches += adaptive && ld > 16 ? 2 : 1;
-  // propagate(padded[i], padded[j]): x = member i (columns), y = member j (rows)
-  PairSet ps{c.xinc.as<double>(), c.xinc.as<double>(), len * ld, len * ld, static_cast<int>(cnt),
-             static_cast<int>(cnt), static_cast<int>(dim), static_cast<int>(ld)};
-  std::vector<int> ords, conv;
-  if (adaptive) {
-    std::vector<double> h(m);
-    SK_CUDA(cudaMemcpyAsync(h.data(), c.sqn.p, m * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
-    SK_CUDA(cudaStreamSynchronize(c.stream()));
-    if (int rc = adaptive_orders(c, ps, h, h, pi, pj, tol, ords, conv, st)) return rc;
-  } else {
-    ords.assign(np, order);
-    conv.assign(np, 1);
-  }
+  GramCore g;
   const bool want_max = scan_products != 0;
-  SK_CUDA(c.err.ensure(np * sizeof(unsigned long long)));
-  SK_CUDA(cudaMemsetAsync(c.err.p, 0xff, np * sizeof(unsigned long long), c.stream()));
-  SK_CUDA(cudaMemsetAsync(c.values.p, 0xff, np * sizeof(double), c.stream()));
-  if (want_max) {
-    SK_CUDA(c.maxr.ensure(np * sizeof(unsigned long long)));
-    SK_CUDA(cudaMemsetAsync(c.maxr.p, 0, np * sizeof(unsigned long long), c.stream()));
-  }
-  Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(),
-            want_max ? c.maxr.as<unsigned long long>() : nullptr, nullptr, nullptr, 0, 0};
-  std::vector<int> distinct(ords.begin(), ords.end());
-  std::sort(distinct.begin(), distinct.end());
-  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
-  for (int ord : distinct) {
-    std::vector<uint32_t> gx, gy, go;
-    for (size_t k = 0; k < np; ++k)
-      if (ords[k] == ord) {
-        gx.push_back(pi[k]);
-        gy.push_back(pj[k]);
-        go.push_back(pout[k]);
-      }
-    if (int rc = run_sweeps(c, ps, gx, gy, go, ord, flags, o, st)) return rc;
-  }
-  std::vector<double> hv(np);
-  std::vector<unsigned long long> he(np), hm(want_max ? np : 0);
-  SK_CUDA(cudaMemcpyAsync(hv.data(), c.values.p, np * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
-  SK_CUDA(cudaMemcpyAsync(he.data(), c.err.p, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream()));
-  if (want_max)
-    SK_CUDA(cudaMemcpyAsync(hm.data(), c.maxr.p, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            c.stream()));
-  SK_CUDA(cudaStreamSynchronize(c.stream()));
-  SK_CUDA(cudaGetLastError());
-  if (int rc = recheck_failures(c, ps, pi, pj, ords, flags, o, hv, he, st)) return rc;
+  if (int rc = gram_core(c, c.raw_x.as<double>(), m, len, dim, adaptive, order, tol, flags, want_max, t0, t1, g, st))
+    return rc;
   double best = 0.0;
-  int first_fatal = -1;
-  for (size_t t = 0; t < np; ++t) {
-    const size_t i = pi[t], j = pj[t];
-    double v = hv[t];
-    if (he[t] != ~0ull) {
-      v = std::numeric_limits<double>::quiet_NaN();
-      if ((he[t] & 3ull) == kErrCorner) {
-        if (first_fatal < 0) first_fatal = static_cast<int>(t);
-      } else if (entry_status) {
-        const auto xi = host_increments(family + i * len * dim, len, dim);
-        const auto yi = host_increments(family + j * len * dim, len, dim);
-        decode_err(he[t], &entry_status[i * m + j], xi.data(), yi.data(), dim);
-      }
-    }
-    if (values) {
-      values[i * m + j] = v;
-      values[j * m + i] = v;
-    }
-    if (orders) {
-      orders[i * m + j] = ords[t];
-      orders[j * m + i] = ords[t];
-    }
+  for (size_t t = 0; t < g.pi.size(); ++t) {
+    const size_t i = g.pi[t], j = g.pj[t];
+    const double v = g.he[t] != ~0ull ? std::numeric_limits<double>::quiet_NaN() : g.hv[t];
+    if (values) values[i * m + j] = values[j * m + i] = v;
+    if (orders) orders[i * m + j] = orders[j * m + i] = g.ords[t];
     if (want_max) {
       double mr;
-      std::memcpy(&mr, &hm[t], sizeof mr);
-      if (pair_max) {
-        pair_max[i * m + j] = mr;
-        pair_max[j * m + i] = mr;
-      }
+      std::memcpy(&mr, &g.hm[t], sizeof mr);
+      if (pair_max) pair_max[i * m + j] = pair_max[j * m + i] = mr;
       if (best < mr) best = mr;
     }
-    if (converged && !conv[t]) *converged = 0;
+    if (converged && !g.conv[t]) *converged = 0;
   }
   if (max_product) *max_product = best;
-  if (first_fatal >= 0) return decode_err(he[first_fatal], st, nullptr, nullptr, dim);
+  if (n_failures) *n_failures = c.failures.size();
   return SK_OK;
+}
+
+int sk_gram_device(const double* d_family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
+                   uint32_t flags, int scan_products, size_t first, size_t last, double* d_matrix,
+                   double* max_product, int* converged, size_t* n_failures, sk_status* st) {
+  clear_status(st);
+  if (n_failures) *n_failures = 0;
+  if (max_product) *max_product = 0.0;
+  if (converged) *converged = 1;
+  if (int rc = gram_validate(m, len, dim, adaptive, order, tol, st)) return rc;
+  if (first > last || last > m * (m + 1) / 2)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "gram_matrix: pair range [%zu, %zu) outside [0, %zu)", first,
+                      last, m * (m + 1) / 2);
+  Ctx* cp = nullptr;
+  if (int rc = get_ctx(&cp, st)) return rc;
+  Ctx& c = *cp;
+  c.failures.clear();
+  if (first == last) return SK_OK;
+  GramCore g;
+  const bool want_max = scan_products != 0;
+  if (int rc = gram_core(c, d_family, m, len, dim, adaptive, order, tol, flags, want_max, first, last, g, st))
+    return rc;
+  // values (NaN for failed entries) into the mirrored matrix cells
+  const size_t np = g.pi.size();
+  SK_CUDA(c.gpairs.ensure(2 * np * sizeof(uint32_t)));
+  SK_CUDA(cudaMemcpyAsync(c.gpairs.p, g.pi.data(), np * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream()));
+  SK_CUDA(cudaMemcpyAsync(c.gpairs.as<uint32_t>() + np, g.pj.data(), np * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                          c.stream()));
+  SK_CUDA(launch_scatter_gram(c.gpairs.as<uint32_t>(), c.gpairs.as<uint32_t>() + np, np, m, c.values.as<double>(),
+                              c.err.as<unsigned long long>(), d_matrix, c.stream()));
+  ++c.aux_launches;
+  double best = 0.0;
+  for (size_t t = 0; t < np; ++t) {
+    if (want_max) {
+      double mr;
+      std::memcpy(&mr, &g.hm[t], sizeof mr);
+      if (best < mr) best = mr;
+    }
+    if (converged && !g.conv[t]) *converged = 0;
+  }
+  if (max_product) *max_product = best;
+  if (n_failures) *n_failures = c.failures.size();
+  SK_CUDA(cudaStreamSynchronize(c.stream()));  // g's host arrays back the pair-list upload
+  return SK_OK;
+}
+
+size_t sk_gram_failures(sk_gram_failure* out, size_t cap) {
+  sk_status st;
+  Ctx* c = nullptr;
+  if (get_ctx(&c, &st)) return 0;
+  const size_t n = std::min(cap, c->failures.size());
+  if (out) std::copy(c->failures.begin(), c->failures.begin() + n, out);
+  return n;
 }
 
 // ------------------------------------------------------ multi-GPU strips
@@ -1253,7 +1347,10 @@ int sk_exchange_alloc(size_t lx, int order, void** abuf, void** prog, sk_status*
   const size_t bytes = (lx - 1) * np_of(order) * sizeof(double);
   SK_CUDA(cudaMalloc(abuf, bytes));
   SK_CUDA(cudaMalloc(prog, 256));
-  SK_CUDA(cudaMemset(*prog, 0, 256));
+  // zeroed on the context's (non-blocking) stream and waited for: a legacy-
+  // stream memset would not be ordered against the sweeps
+  SK_CUDA(cudaMemsetAsync(*prog, 0, 256, cp->stream()));
+  SK_CUDA(cudaStreamSynchronize(cp->stream()));
   return SK_OK;
 }
 
@@ -1261,7 +1358,8 @@ int sk_exchange_reset(void* prog, sk_status* st) {
   clear_status(st);
   Ctx* cp = nullptr;
   if (int rc = get_ctx(&cp, st)) return rc;
-  SK_CUDA(cudaMemset(prog, 0, 256));
+  SK_CUDA(cudaMemsetAsync(prog, 0, 256, cp->stream()));
+  SK_CUDA(cudaStreamSynchronize(cp->stream()));
   return SK_OK;
 }
 
@@ -1386,9 +1484,7 @@ int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, s
   if (diag) SK_CUDA(cudaMemcpyAsync(diag, d_diag, nd * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
   SK_CUDA(cudaStreamSynchronize(c.stream()));
   if (key != ~0ull) {
-    const auto xi = host_increments(x, lx, dim);
-    const auto yi = host_increments(y, ly, dim);
-    return decode_err(key, st, xi.data(), yi.data(), dim);
+    return decode_err(key, st, device_delta(c, c.xinc.as<double>(), c.yinc.as<double>(), ld, dim, key));
   }
   if (band_end == bands && value) *value = v;
   return SK_OK;
@@ -1441,7 +1537,7 @@ int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, s
     cudaMemcpyAsync(&key, c.err.p, sizeof key, cudaMemcpyDeviceToHost, c.stream());
     cudaMemcpyAsync(value, c.values.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream());
     if (cudaError_t e = cudaStreamSynchronize(c.stream()); e != cudaSuccess) { rc = cuda_fail(st, e, "sync"); break; }
-    if (key != ~0ull) rc = decode_err(key, st, nullptr, nullptr, dim);
+    if (key != ~0ull) rc = decode_err(key, st, device_delta(c, c.xinc.as<double>(), c.yinc.as<double>(), ld, dim, key));
   } while (false);
   sk_exchange_free(xa, xp);
   return rc;
@@ -1499,7 +1595,7 @@ int sk_stats_reset(void) {
     cudaEventDestroy(r.b);
   }
   c->stats.clear();
-  c->sweep_launches = c->aux_launches = c->table_launches = c->paired_launches = 0;
+  c->sweep_launches = c->aux_launches = c->table_launches = c->literal_rechecks = 0;
   c->done_ms = c->done_tiles = c->done_flops = c->done_table_ms = 0.0;
   return SK_OK;
 }
@@ -1529,7 +1625,7 @@ int sk_stats_get(sk_stats* out) {
   out->tiles = c->done_tiles;
   out->tile_flops = c->done_flops;
   out->table_launches = c->table_launches;
-  out->paired_launches = c->paired_launches;
+  out->literal_rechecks = c->literal_rechecks;
   out->table_ms = c->done_table_ms;
   return SK_OK;
 }

@@ -44,14 +44,24 @@ __device__ __forceinline__ unsigned long long err_key(unsigned i, unsigned j, un
   return (static_cast<unsigned long long>(i + j) << 32) | (static_cast<unsigned long long>(i) << 2) | code;
 }
 
-// tile_series.cpp:70-75
-// |a0 - b0| > 1e-9 max(1, |a0|, |b0|), as three comparisons: scaling by a
-// positive constant is monotone under rounding, so this is the same
-// predicate (NaN operands compare false in both forms), without the
-// fmax select chains and branches
-__device__ __forceinline__ bool corner_mismatch(double a0, double b0) {
+// tile_series.cpp:70-75: |a0 - b0| > tol max(1, |a0|, |b0|), tol = 1e-9, as
+// three comparisons: scaling by a positive constant is monotone under
+// rounding, so this is the same predicate (NaN operands compare false in both
+// forms), without the fmax select chains and branches.
+//
+// Only the literal kernel (N = 0), whose alpha0 / beta0 are the reference's
+// bits, decides the reference's throw.  The register kernels round alpha0 and
+// beta0 differently, so in strict mode they SCREEN at a 100x tighter
+// tolerance and the host re-sweeps every screened pair with the literal
+// kernel (recheck_failures): the throw, its tile and a returned value are then
+// exactly the reference's.  Brownian inputs sit far below the screen
+// (cfg 5 self-kernels: 5e-13, tests/golden/scale.json), so no clean pair
+// pays for a re-sweep.
+constexpr double kCornerTol = 1e-9;
+constexpr double kCornerScreen = 1e-11;
+__device__ __forceinline__ bool corner_mismatch(double a0, double b0, double tol) {
   const double d = fabs(a0 - b0);
-  return (d > 1e-9) & (d > 1e-9 * fabs(a0)) & (d > 1e-9 * fabs(b0));
+  return (d > tol) & (d > tol * fabs(a0)) & (d > tol * fabs(b0));
 }
 
 // Sequential non-FMA dot product in coordinate order: bit-identical to
@@ -122,69 +132,6 @@ __device__ __forceinline__ void tile_powers(double delta, double (&ph)[N + 1], d
     p[1] = delta;
 #pragma unroll
     for (int m = 2; m < n; ++m) p[m] = ph[m] * kFactRatio<N>(m);
-  }
-}
-
-// alpha' alone (the paired-band kernel's alpha warp), powers precomputed
-// (tile_powers): the same expressions, in the same order, as
-// tile_update_scaled, so the bits are identical
-template <int N>
-__device__ __forceinline__ void tile_alpha_scaled(const double (&q)[N + 1], const double (&r)[N + 1],
-                                                  const double (&ph)[N + 1], const double (&p)[N + 1], double delta,
-                                                  double (&qo)[N + 1], bool fault) {
-  constexpr int n = N + 1;
-  double v[N > 0 ? N : 1];
-#pragma unroll
-  for (int a = 0; a < N; ++a) {
-    double acc = r[1];
-#pragma unroll
-    for (int k = 2; k <= N - a; ++k) acc = fma(acc, static_cast<double>(a + k), r[k]);
-    v[a] = acc;
-  }
-#pragma unroll
-  for (int a = 0; a < n; ++a) qo[a] = q[a];
-#pragma unroll
-  for (int b = 1; b < n; ++b)
-#pragma unroll
-    for (int a = b; a < n; ++a) qo[a] = fma(q[a - b], p[b], qo[a]);
-#pragma unroll
-  for (int a = 0; a < N; ++a) qo[a] = fma(ph[a], v[a], qo[a]);
-  if constexpr (N >= 1) {
-    if (fault) {
-      const double c11 = 2.0 * q[0] * delta;
-      qo[1] -= c11;
-    }
-  }
-}
-
-// beta' alone (the paired-band kernel's beta warp), bit-identical likewise
-template <int N>
-__device__ __forceinline__ void tile_beta_scaled(const double (&q)[N + 1], const double (&r)[N + 1],
-                                                 const double (&ph)[N + 1], const double (&p)[N + 1], double delta,
-                                                 double (&ro)[N + 1], bool fault) {
-  constexpr int n = N + 1;
-  double u[n];
-#pragma unroll
-  for (int b = 0; b < n; ++b) {
-    double acc = q[0];
-#pragma unroll
-    for (int k = 1; k <= N - b; ++k) acc = fma(acc, static_cast<double>(b + k), q[k]);
-    u[b] = acc;
-  }
-#pragma unroll
-  for (int c = 1; c < n; ++c) ro[c] = r[c];
-#pragma unroll
-  for (int b = 1; b < n; ++b)
-#pragma unroll
-    for (int c = b + 1; c < n; ++c) ro[c] = fma(r[c - b], p[b], ro[c]);
-  ro[0] = ph[0] * u[0];
-#pragma unroll
-  for (int b = 1; b < n; ++b) ro[b] = fma(ph[b], u[b], ro[b]);
-  if constexpr (N >= 1) {
-    if (fault) {
-      const double c11 = 2.0 * q[0] * delta;
-      ro[1] -= c11;
-    }
   }
 }
 

@@ -44,6 +44,11 @@ cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint3
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
                              int dim, int ld, bool exact, double* tab, unsigned long long tab_stride,
                              cudaStream_t st);
+cudaError_t launch_reset_slots(const uint32_t* idx, size_t n, unsigned long long* err, cudaStream_t st);
+cudaError_t launch_gather_slots(const uint32_t* idx, size_t n, const double* values, const unsigned long long* err,
+                                unsigned long long* out, cudaStream_t st);
+cudaError_t launch_scatter_gram(const uint32_t* pi, const uint32_t* pj, size_t n, size_t m, const double* values,
+                                const unsigned long long* err, double* mat, cudaStream_t st);
 cudaError_t launch_grid_init(double* grid, size_t nout, size_t lx, size_t ly, cudaStream_t st);
 cudaError_t launch_step_tile_literal(double delta, int order, const double* w65, const double* in, double* out,
                                      cudaStream_t st);
@@ -54,11 +59,8 @@ cudaError_t launch_step_tile_fast(double delta, int order, const double* in, dou
 // exact: reference-identical delta (sequential non-FMA dot) + per-pair
 // max|delta| tracking; otherwise an FMA dot and no max tracking.
 // extras: knot grid / diagonal outputs.
-// paired: two-warp bands (alpha warp + beta warp per band; streaming schedule,
-// register kernels, no exact max) for launches that leave most SM
-// sub-partitions idle: about half the per-step latency of a one-warp band.
-cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream,
+cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, int grid, cudaStream_t stream,
                          const SweepParams& P);
-cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
+cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, int* blocks_per_sm);
 
 }  // namespace skb

@@ -55,30 +55,24 @@ constexpr int kSweepWarps = SK_SWEEP_WARPS;
 // SM sub-partition holds 16K registers, so <= 168 registers/thread gives 3
 // warps per sub-partition (12 per SM), more gives only 2.  Orders up to 10
 // fit 168 without spills; larger orders keep the unconstrained allocation.
-#ifndef SK_ROWS_PER_LANE
-#define SK_ROWS_PER_LANE 1
-#endif
 #ifndef SK_MIN_BLOCKS
 #define SK_MIN_BLOCKS 0
 #endif
 __host__ __device__ constexpr int sweep_min_blocks(int N) {
-  return SK_MIN_BLOCKS > 0 ? SK_MIN_BLOCKS : (N >= 1 && N <= 10 ? (SK_ROWS_PER_LANE == 2 ? 8 : 12) : 1);
+  return SK_MIN_BLOCKS > 0 ? SK_MIN_BLOCKS : (N >= 1 && N <= 10 ? 12 : 1);
 }
 
-// Rows per lane.  R = 2: a warp sweeps a 64-row band, lane t owning rows t
-// and t + 32 (the second tile 32 columns behind the first), so two
-// independent tiles per step share the per-step overhead.  Measured on B200
-// (N = 8, d = 8, 256 x 4096^2): R = 1 68 ms, R = 2 77 ms (200 registers, 8
-// warps/SM, smaller chunks) -- R = 1 is the default; the literal kernel
-// (N = 0, series in local memory) always uses R = 1.
-__host__ __device__ constexpr int rows_per_lane(int N) { return N > 0 ? SK_ROWS_PER_LANE : 1; }
+// Rows per lane: one tile row per lane, 32-row bands.  (Two rows per lane --
+// 64-row bands, two independent tiles per step -- measured slower on B200:
+// N = 8, d = 8, 256 x 4096^2: 77 vs 68 ms at 200 registers and 8 warps/SM.)
+__host__ __device__ constexpr int rows_per_lane(int) { return 1; }
 // columns per staging group / delta batch
 #ifndef SK_CHUNK
 #define SK_CHUNK 16
 #endif
-__host__ __device__ constexpr int chunk_cols(int R) { return R == 2 ? 8 : SK_CHUNK; }
-// dx ring rows (power of two >= 32 R + 2 chunk)
-__host__ __device__ constexpr int ring_rows(int R) { return R == 2 ? 128 : 64; }
+__host__ __device__ constexpr int chunk_cols(int) { return SK_CHUNK; }
+// dx ring rows (power of two >= 32 + 2 chunks)
+__host__ __device__ constexpr int ring_rows(int) { return 64; }
 
 struct SweepParams {
   const double* xinc;             // increments of the column series (first series, x)
@@ -162,6 +156,9 @@ constexpr unsigned kFlagWFault = 4u;
 // the host sweeps any pair that ends non-finite or flagged again with this
 // bit set, which reports the reference's first failing tile exactly.
 constexpr unsigned kFlagAllTotals = 1u << 8;
+// Internal: run the literal (bit-identical) kernel whatever the order -- the
+// strict-corner re-sweep of pairs the register kernels screened.
+constexpr unsigned kFlagLiteral = 1u << 9;
 
 __host__ __device__ constexpr int series_len(int N) { return N > 0 ? N + 1 : kMaxOrder + 1; }
 __host__ __device__ constexpr int col_stride(int N) { return (series_len(N) + 1) & ~1; }
@@ -315,7 +312,7 @@ __device__ __forceinline__ void sts_series(double* dst, const double (&v)[NA], i
 // waiting on the band below's progress counter.  Segment mode: one segment,
 // all inputs complete; `restore` loads the band's lane state from its record
 // (not the band's first segment), `save` stores it (not the last).
-template <int N, int DP, bool EXACT, bool EXTRAS, bool PAIRED = false>
+template <int N, int DP, bool EXACT, bool EXTRAS>
 __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsigned b, int lane,
                                           double* __restrict__ smem, int c_begin, int c_end, bool restore,
                                           bool save) {
@@ -333,19 +330,11 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // registers allow it: d <= 8, register kernels, no exact max.  Measured:
   // 256 x 4096^2 62.95 vs 63.5 ms; at d = 16 it spills and gains nothing.
   constexpr bool kInlineDelta = SK_INLINE_DELTA && DP > 0 && DP <= 8 && N > 0 && !EXACT && R == 1;
-  static_assert(!PAIRED || (N > 0 && !EXACT && R == 1), "paired bands: register kernels, R = 1, no exact max");
-  // paired bands (sweep_pair_kernel): warp 0 of the CTA is the alpha warp --
-  // waits, staging, alpha', totals, checks, outputs -- and warp 1 the beta
-  // warp (beta' only); every step they swap the halves through parity-double-
-  // buffered shared slots and one CTA barrier
-  const bool beta_warp = PAIRED && (threadIdx.x >> 5) == 1;
   double* s_alpha = smem;                                   // 2 x K x NP
   double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
   double* s_out = s_pass + 32 * R * NP;                     // K x NP
   double* s_ring = s_out + (direct_top_out(DP) ? 0 : kStage);  // RING x XS (DP > 0)
   double* s_delta = s_ring + (DP > 0 ? RING * XS : 0);      // [buf][r][k][lane]
-  double* s_pass2 = smem + stage_doubles_per_warp(N, DP);   // PAIRED: odd-step alpha slots (32 x NP)
-  double* s_r = s_pass2 + 32 * NP;                          // PAIRED: beta slots, 2 parities x 32 x NP
   const int n = N > 0 ? N + 1 : P.order + 1;
   const int rows = P.rows, cols = P.cols;
   const int row0 = static_cast<int>(b) * 32 * R;
@@ -370,13 +359,6 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const bool all_totals = EXTRAS || N == 0 || (P.flags & kFlagAllTotals) != 0;
   const bool band_top = row0 + 32 * R >= rows;  // the band holds the pair's last row
   const bool streaming = P.seg_cols == 0;
-  // PAIRED: both warps of the band leave together (the alpha warp decides)
-  auto agree = [&](bool ok) {
-    if constexpr (PAIRED)
-      return __syncthreads_and(ok ? 1 : 0) != 0;
-    else
-      return ok;
-  };
   double* const rec = streaming ? nullptr
                                 : P.susp + (static_cast<size_t>(slot) * P.bands + b) *
                                                static_cast<size_t>(susp_record_doubles(N));
@@ -386,10 +368,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // pair's first unit is queued only once the previous pair has finished.)
   if (streaming && b == 0 && has_above && p >= static_cast<unsigned>(P.slots)) {
     unsigned long long seen0 = 0;
-    const bool ok = beta_warp || wait_progress(P, prog_row + (P.bands - 1),
-                                               static_cast<unsigned long long>(p - P.slots) * (cols + 1) + cols,
-                                               seen0, p, b);
-    if (!agree(ok)) return kBandAbort;
+    if (!wait_progress(P, prog_row + (P.bands - 1), static_cast<unsigned long long>(p - P.slots) * (cols + 1) + cols,
+                       seen0, p, b))
+      return kBandAbort;
   }
 
   // per tile r of this lane: row i_r = row0 + 32 r + lane, column s - lane - 32 r
@@ -482,7 +463,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     }
     cp_async_commit();
   };
-  if (!has_below && !beta_warp) {
+  if (!has_below) {
     // band 0: the bottom edge of the domain is the unit series in every column
     for (int e = lane; e < 2 * kStage; e += 32) s_alpha[e] = (e % NP == 0) ? 1.0 : 0.0;
   }
@@ -495,18 +476,15 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       for (int m = 0; m < NA; ++m)
         if (NA <= kMaxRegOrder + 1 || m < n) roA[r][m] = rec[(r * NP + m) * 32 + lane];
     for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = rec[32 * R * NP + e];
-  } else if (!beta_warp) {
-    for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
   } else {
-    // PAIRED beta warp: every tile's beta before its first column (step 0, parity 0)
-    for (int e = lane; e < 32 * NP; e += 32) s_r[e] = (e % NP == 0) ? 1.0 : 0.0;
+    for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
   }
   if constexpr (DP > 0) {
     // dx of the columns the lanes still need behind the first staged group,
     // [c K - 32 R, c K): zero below column 0 (zero increments => delta = 0,
     // which keeps a tile's beta at the unit series before its first column)
     const int h0 = c_begin * K - 32 * R;
-    for (int e = beta_warp ? 32 * R * (DP / 2) : lane; e < 32 * R * (DP / 2); e += 32) {
+    for (int e = lane; e < 32 * R * (DP / 2); e += 32) {
       const int c = e / (DP / 2), part = e - c * (DP / 2);
       const int col = h0 + c;
       double* dst = s_ring + (col & (RING - 1)) * XS + 2 * part;
@@ -522,12 +500,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // start no closer than start_lag columns behind the band below: bands of
   // one pair then run evenly spread in time instead of bunched at the
   // minimum hand-over distance, where every timing jitter becomes a wait
-  {
-    const bool ok = beta_warp || !(streaming && has_below) ||
-                    wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin);
-    if (!agree(ok)) return kBandAbort;
-  }
-  if (!beta_warp) stage_group(c_begin);
+  if (streaming && has_below && !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin))
+    return kBandAbort;
+  stage_group(c_begin);
 
   // one step = R tiles of this lane (one basic block, conditional work predicated)
   auto step = [&](bool TOT, int s, int k, const double* stage, const double* dl, double (&r_in)[R][NA],
@@ -595,7 +570,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       // the reference's throw order inside a tile: delta guard (checked when
       // the chunk's deltas are formed), corner check, non-finite total
       // (wavefront.cpp:150-173); the first failing tile of the row wins
-      const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0]);
+      const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0], N > 0 ? kCornerScreen : kCornerTol);
       const bool nf = (TOT || N == 0) && !isfinite(total);
       const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
       const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
@@ -723,174 +698,50 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     }
   };
 
-  if constexpr (!PAIRED) {
-    for (int c0 = c_begin * K, chunk = c_begin; c0 < steps && chunk < c_end; c0 += K, ++chunk) {
-      __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
-      if (chunk + 1 < ngroups && chunk + 1 < c_end) {
-        if (streaming && has_below &&
-            !wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin))
-          return kBandAbort;
-        stage_group(chunk + 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      const double* stage = s_alpha + (chunk & 1) * kStage;
-      const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * R * K * 32);
-      const int kend = min(K, steps - c0);
-      form_deltas(c0, kend, dl);
-      __syncwarp();
-      auto run_chunk = [&](bool tot) {
-        int k = 0;
-#pragma unroll 1
-        for (; k + 1 < kend; k += 2) {
-          step(tot, c0 + k, k, stage, dl, roA, roB);
-          step(tot, c0 + k + 1, k + 1, stage, dl, roB, roA);
-        }
-        if (k < kend) {
-          step(tot, c0 + k, k, stage, dl, roA, roB);
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int m = 0; m < NA; ++m) roA[r][m] = roB[r][m];
-        }
-      };
-      // totals where the pair's final tile can fall (or everywhere, kFlagAllTotals)
-      if constexpr (EXTRAS || N == 0) {
-        run_chunk(true);
-      } else {
-        if (all_totals || (band_top && c0 + K > cols - 1))
-          run_chunk(true);
-        else
-          run_chunk(false);
-      }
-      hand_up(c0, kend);
+  for (int c0 = c_begin * K, chunk = c_begin; c0 < steps && chunk < c_end; c0 += K, ++chunk) {
+    __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
+    if (chunk + 1 < ngroups && chunk + 1 < c_end) {
+      if (streaming && has_below &&
+          !wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin))
+        return kBandAbort;
+      stage_group(chunk + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-  } else {
-    // paired band: R = 1, streaming.  Step s reads alpha from parity s & 1
-    // of the slots and writes parity (s + 1) & 1, so one CTA barrier per step
-    // both publishes the step's halves and retires the reads of step s - 1.
-    // A step's increment product and its powers depend on no other tile:
-    // they are formed one step ahead (within a chunk), off the step's
-    // dependency chain, which a lone warp cannot hide behind other warps.
-    auto delta_at = [&](int s, int k, const double* dl) -> double {
-      if constexpr (kInlineDelta) {
-        const double* xr = s_ring + ((s - lane) & (RING - 1)) * XS;
-        double e0 = 0.0, e1 = 0.0;
+    __syncwarp();
+    const double* stage = s_alpha + (chunk & 1) * kStage;
+    const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * R * K * 32);
+    const int kend = min(K, steps - c0);
+    form_deltas(c0, kend, dl);
+    __syncwarp();
+    auto run_chunk = [&](bool tot) {
+      int k = 0;
+#pragma unroll 1
+      for (; k + 1 < kend; k += 2) {
+        step(tot, c0 + k, k, stage, dl, roA, roB);
+        step(tot, c0 + k + 1, k + 1, stage, dl, roB, roA);
+      }
+      if (k < kend) {
+        step(tot, c0 + k, k, stage, dl, roA, roB);
 #pragma unroll
-        for (int c = 0; c < DP; c += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(xr + c);
-          e0 = fma(v.x, dyr[0][c], e0);
-          e1 = fma(v.y, dyr[0][c + 1], e1);
-        }
-        return e0 + e1;
-      } else {
-        return dl[k * 32 + lane];
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int m = 0; m < NA; ++m) roA[r][m] = roB[r][m];
       }
     };
-    auto step2 = [&](bool TOT, int s, int k, const double* stage, double delta, const double (&ph)[NA],
-                     const double (&pw)[NA], double (&r_in)[NA], double (&ro_out)[NA]) {
-      const int par = s & 1;
-      const double* sp_rd = par ? s_pass2 : s_pass;
-      double* sp_wr = par ? s_pass : s_pass2;
-      double q[NA];
-      lds_series<NA>(lane == 0 ? stage + k * NP : sp_rd + (lane - 1) * NP, q, n);
-      const int j = s - lane;
-      if (beta_warp) {
-        tile_beta_scaled<N>(q, r_in, ph, pw, delta, ro_out, fault);
-        sts_series<NA>(s_r + ((par ^ 1) * 32 + lane) * NP, ro_out, n);
-      } else {
-        double r[NA], qo[NA];
-        lds_series<NA>(s_r + (par * 32 + lane) * NP, r, n);
-        const bool act = row_ok[0] && j >= 0 && j < cols;
-        if constexpr (kInlineDelta)
-          jkey[0] = min(jkey[0], (act && !(fabs(delta) <= kDeltaOverflowLimit))
-                                     ? (static_cast<unsigned>(j) << 2) | kErrDelta
-                                     : ~0u);
-        tile_alpha_scaled<N>(q, r, ph, pw, delta, qo, fault);
-        double total = 0.0;
-        if (TOT) total = scaled_total<N>(qo);
-        if constexpr (direct_top_out(DP)) {
-          sts_series<NA>(sp_wr + lane * NP, qo, n);
-          const bool up = has_above && lane == 31 && j >= 0 && j < cols;
-          double* dst = out_buf + static_cast<size_t>(up ? j : 0) * NP;
-#pragma unroll
-          for (int m = 0; m < NA; m += 2) st_global_cg2_if(up, dst + m, qo[m], m + 1 < NA ? qo[m + 1] : 0.0);
-        } else {
-          sts_series<NA>(lane == 31 ? s_out + k * NP : sp_wr + lane * NP, qo, n);
-        }
-        const bool cm = strict & corner_mismatch(q[0], r[0]);
-        const bool nf = TOT && !isfinite(total);
-        const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
-        const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
-        jkey[0] = min(jkey[0], (act && code != 0u) ? kk : ~0u);
-        if (TOT) st_global_if(last_row[0] && j == cols - 1, P.values + out, total);
-        if constexpr (EXTRAS) {
-          if (P.grid)
-            st_global_if(act, P.grid + out * P.grid_stride + static_cast<size_t>(j + 1) * (rows + 1) + (irow[0] + 1),
-                         total);
-          if (P.diag) st_global_if(act && irow[0] == j, P.diag + out * P.diag_stride + irow[0], total);
-        }
-      }
-      __syncthreads();
-    };
-    for (int c0 = c_begin * K, chunk = c_begin; c0 < steps && chunk < c_end; c0 += K, ++chunk) {
-      __syncthreads();  // both warps are done with the buffers group chunk + 1 overwrites
-      bool ok = true;
-      if (!beta_warp) {
-        if (chunk + 1 < ngroups && chunk + 1 < c_end) {
-          ok = !(streaming && has_below) || wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin);
-          if (ok) {
-            stage_group(chunk + 1);
-            cp_async_wait<1>();
-          }
-        } else {
-          cp_async_wait<0>();
-        }
-      }
-      if (!agree(ok)) return kBandAbort;  // also hands the staged group to the beta warp
-      const double* stage = s_alpha + (chunk & 1) * kStage;
-      const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * K * 32);
-      const int kend = min(K, steps - c0);
-      if constexpr (!kInlineDelta) {
-        if (!beta_warp) form_deltas(c0, kend, dl);
-        __syncthreads();
-      }
-      auto run_chunk = [&](bool tot) {
-        double d0 = delta_at(c0, 0, dl), ph0[NA], pw0[NA];
-        tile_powers<N>(d0, ph0, pw0);
-        int k = 0;
-#pragma unroll 1
-        for (; k + 1 < kend; k += 2) {
-          const double d1 = delta_at(c0 + k + 1, k + 1, dl);
-          double ph1[NA], pw1[NA];
-          tile_powers<N>(d1, ph1, pw1);
-          step2(tot, c0 + k, k, stage, d0, ph0, pw0, roA[0], roB[0]);
-          if (k + 2 < kend) {
-            d0 = delta_at(c0 + k + 2, k + 2, dl);
-            tile_powers<N>(d0, ph0, pw0);
-          }
-          step2(tot, c0 + k + 1, k + 1, stage, d1, ph1, pw1, roB[0], roA[0]);
-        }
-        if (k < kend) {
-          step2(tot, c0 + k, k, stage, d0, ph0, pw0, roA[0], roB[0]);
-#pragma unroll
-          for (int m = 0; m < NA; ++m) roA[0][m] = roB[0][m];
-        }
-      };
-      if constexpr (EXTRAS) {
+    // totals where the pair's final tile can fall (or everywhere, kFlagAllTotals)
+    if constexpr (EXTRAS || N == 0) {
+      run_chunk(true);
+    } else {
+      if (all_totals || (band_top && c0 + K > cols - 1))
         run_chunk(true);
-      } else {
-        if (all_totals || (band_top && c0 + K > cols - 1))
-          run_chunk(true);
-        else
-          run_chunk(false);
-      }
-      if (!beta_warp) hand_up(c0, kend);
+      else
+        run_chunk(false);
     }
+    hand_up(c0, kend);
   }
-  if (streaming && !has_above && P.bands > 1 && !beta_warp) {
+  if (streaming && !has_above && P.bands > 1) {
     // the last band publishes completion too: the slot's next pair (p + slots)
     // may only rewrite the column buffer once this band has read all of it
     cp_async_wait<0>();
@@ -911,7 +762,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // reductions, so each segment flushes its part
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (jkey[r] != ~0u && !beta_warp) atomicMin(P.err + out, err_key(irow[r], jkey[r] >> 2, jkey[r] & 3u));
+    if (jkey[r] != ~0u) atomicMin(P.err + out, err_key(irow[r], jkey[r] >> 2, jkey[r] & 3u));
   if constexpr (EXACT) {
     if (P.maxrho) {
 #pragma unroll
@@ -1062,39 +913,6 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
         atomicAdd(P.ctr + 2 * kCtrLine, 1u);
       }
     }
-  }
-}
-
-// Paired bands (streaming schedule only): a 64-thread CTA per band, warp 0
-// the alpha warp, warp 1 the beta warp (sweep_band<..., PAIRED = true>).
-// Dynamic shared memory: pair_smem_doubles(N, DP).
-__host__ __device__ constexpr int pair_smem_doubles(int N, int DP) {
-  return stage_doubles_per_warp(N, DP) + 3 * 32 * col_stride(N);
-}
-
-template <int N, int DP, bool EXTRAS>
-__global__ void __launch_bounds__(64) sweep_pair_kernel(const SweepParams P) {
-  extern __shared__ __align__(16) double s_dyn[];
-  __shared__ unsigned s_unit;
-  const int lane = threadIdx.x & 31;
-  const unsigned nb = static_cast<unsigned>(P.band_end - P.band_begin);
-  const unsigned gsz = static_cast<unsigned>(P.group) * nb;
-  for (;;) {
-    // one thread claims the unit (or sees the abort flag) for both warps
-    if (threadIdx.x == 0)
-      s_unit = *reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0 ? ~0u : atomicAdd(P.queue, 1u);
-    __syncthreads();
-    const unsigned u = s_unit;
-    __syncthreads();
-    if (u >= static_cast<unsigned>(P.npairs) * nb) return;
-    const unsigned g = u / gsz;
-    const unsigned rem = u - g * gsz;
-    const unsigned g0 = g * static_cast<unsigned>(P.group);
-    const unsigned gcount = min(static_cast<unsigned>(P.group), static_cast<unsigned>(P.npairs) - g0);
-    const unsigned b = static_cast<unsigned>(P.band_begin) + rem / gcount;
-    const unsigned p = g0 + (rem - (b - static_cast<unsigned>(P.band_begin)) * gcount);
-    if (sweep_band<N, DP, false, EXTRAS, true>(P, p, b, lane, s_dyn, 0, 0x7fffffff, false, false) == kBandAbort)
-      return;
   }
 }
 

@@ -8,84 +8,35 @@
 
 namespace skb {
 
-__attribute__((weak)) cudaError_t sweep_launch_n0(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n0(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n1(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n1(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n2(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n2(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n3(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n3(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n4(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n4(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n5(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n5(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n6(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n6(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n7(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n7(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n8(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n8(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n9(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n9(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n10(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n10(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n11(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n11(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n12(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n12(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n13(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n13(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n14(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n14(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n15(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n15(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
-__attribute__((weak)) cudaError_t sweep_launch_n16(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream, const SweepParams& P);
-__attribute__((weak)) cudaError_t sweep_occupancy_n16(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm);
+#define SK_DECL(n)                                                                                          \
+  __attribute__((weak)) cudaError_t sweep_launch_n##n(int dp, bool exact, bool extras, int grid,           \
+                                                      cudaStream_t stream, const SweepParams& P);           \
+  __attribute__((weak)) cudaError_t sweep_occupancy_n##n(int dp, bool exact, bool extras, int* blocks_per_sm);
+SK_DECL(0) SK_DECL(1) SK_DECL(2) SK_DECL(3) SK_DECL(4) SK_DECL(5) SK_DECL(6) SK_DECL(7) SK_DECL(8)
+SK_DECL(9) SK_DECL(10) SK_DECL(11) SK_DECL(12) SK_DECL(13) SK_DECL(14) SK_DECL(15) SK_DECL(16)
+#undef SK_DECL
 
-cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream,
+#define SK_CASE(n, fn, ...) \
+  case n: return fn##n ? fn##n(__VA_ARGS__) : cudaErrorInvalidValue;
+#define SK_ALL(fn, ...)                                                                                     \
+  SK_CASE(0, fn, __VA_ARGS__) SK_CASE(1, fn, __VA_ARGS__) SK_CASE(2, fn, __VA_ARGS__)                      \
+  SK_CASE(3, fn, __VA_ARGS__) SK_CASE(4, fn, __VA_ARGS__) SK_CASE(5, fn, __VA_ARGS__)                      \
+  SK_CASE(6, fn, __VA_ARGS__) SK_CASE(7, fn, __VA_ARGS__) SK_CASE(8, fn, __VA_ARGS__)                      \
+  SK_CASE(9, fn, __VA_ARGS__) SK_CASE(10, fn, __VA_ARGS__) SK_CASE(11, fn, __VA_ARGS__)                    \
+  SK_CASE(12, fn, __VA_ARGS__) SK_CASE(13, fn, __VA_ARGS__) SK_CASE(14, fn, __VA_ARGS__)                   \
+  SK_CASE(15, fn, __VA_ARGS__) SK_CASE(16, fn, __VA_ARGS__)
+
+cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, int grid, cudaStream_t stream,
                          const SweepParams& P) {
   switch (n_template) {
-    case 0: return sweep_launch_n0 ? sweep_launch_n0(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 1: return sweep_launch_n1 ? sweep_launch_n1(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 2: return sweep_launch_n2 ? sweep_launch_n2(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 3: return sweep_launch_n3 ? sweep_launch_n3(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 4: return sweep_launch_n4 ? sweep_launch_n4(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 5: return sweep_launch_n5 ? sweep_launch_n5(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 6: return sweep_launch_n6 ? sweep_launch_n6(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 7: return sweep_launch_n7 ? sweep_launch_n7(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 8: return sweep_launch_n8 ? sweep_launch_n8(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 9: return sweep_launch_n9 ? sweep_launch_n9(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 10: return sweep_launch_n10 ? sweep_launch_n10(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 11: return sweep_launch_n11 ? sweep_launch_n11(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 12: return sweep_launch_n12 ? sweep_launch_n12(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 13: return sweep_launch_n13 ? sweep_launch_n13(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 14: return sweep_launch_n14 ? sweep_launch_n14(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 15: return sweep_launch_n15 ? sweep_launch_n15(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
-    case 16: return sweep_launch_n16 ? sweep_launch_n16(dp, exact, extras, paired, grid, stream, P) : cudaErrorInvalidValue;
+    SK_ALL(sweep_launch_n, dp, exact, extras, grid, stream, P)
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, bool paired, int* blocks_per_sm) {
+cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, int* blocks_per_sm) {
   switch (n_template) {
-    case 0: return sweep_occupancy_n0 ? sweep_occupancy_n0(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 1: return sweep_occupancy_n1 ? sweep_occupancy_n1(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 2: return sweep_occupancy_n2 ? sweep_occupancy_n2(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 3: return sweep_occupancy_n3 ? sweep_occupancy_n3(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 4: return sweep_occupancy_n4 ? sweep_occupancy_n4(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 5: return sweep_occupancy_n5 ? sweep_occupancy_n5(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 6: return sweep_occupancy_n6 ? sweep_occupancy_n6(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 7: return sweep_occupancy_n7 ? sweep_occupancy_n7(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 8: return sweep_occupancy_n8 ? sweep_occupancy_n8(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 9: return sweep_occupancy_n9 ? sweep_occupancy_n9(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 10: return sweep_occupancy_n10 ? sweep_occupancy_n10(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 11: return sweep_occupancy_n11 ? sweep_occupancy_n11(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 12: return sweep_occupancy_n12 ? sweep_occupancy_n12(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 13: return sweep_occupancy_n13 ? sweep_occupancy_n13(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 14: return sweep_occupancy_n14 ? sweep_occupancy_n14(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 15: return sweep_occupancy_n15 ? sweep_occupancy_n15(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
-    case 16: return sweep_occupancy_n16 ? sweep_occupancy_n16(dp, exact, extras, paired, blocks_per_sm) : cudaErrorInvalidValue;
+    SK_ALL(sweep_occupancy_n, dp, exact, extras, blocks_per_sm)
     default: return cudaErrorInvalidValue;
   }
 }

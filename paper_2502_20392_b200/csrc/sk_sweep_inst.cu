@@ -80,57 +80,6 @@ static cudaError_t occupancy_one(int* blocks_per_sm) {
                                                        kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>());
 }
 
-#if SK_N > 0
-// paired-band kernels (sk_sweep.cuh sweep_pair_kernel): streaming, no exact max
-template <int N, int DP, bool EXTRAS>
-static cudaError_t prepare_pair() {
-  static std::atomic<unsigned long long> done_mask{0};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
-  const size_t smem = pair_smem_doubles(N, DP) * sizeof(double);
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(sweep_pair_kernel<N, DP, EXTRAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  e = cudaFuncSetAttribute(sweep_pair_kernel<N, DP, EXTRAS>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
-  if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_acq_rel);
-  return e;
-}
-
-template <int N, int DP, bool EXTRAS>
-static cudaError_t launch_pair(int grid, cudaStream_t stream, const SweepParams& P) {
-  cudaError_t e = prepare_pair<N, DP, EXTRAS>();
-  if (e != cudaSuccess) return e;
-  sweep_pair_kernel<N, DP, EXTRAS><<<grid, 64, pair_smem_doubles(N, DP) * sizeof(double), stream>>>(P);
-  return cudaGetLastError();
-}
-
-template <int N, int DP, bool EXTRAS>
-static cudaError_t occupancy_pair(int* blocks_per_sm) {
-  cudaError_t e = prepare_pair<N, DP, EXTRAS>();
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_pair_kernel<N, DP, EXTRAS>, 64,
-                                                       pair_smem_doubles(N, DP) * sizeof(double));
-}
-
-#define SK_PAIR_SWITCH(FN, ...)                                                                   \
-  switch (dp) {                                                                                   \
-    case 0: return extras ? FN<SK_N, 0, true>(__VA_ARGS__) : FN<SK_N, 0, false>(__VA_ARGS__);     \
-    case 2: return extras ? FN<SK_N, 2, true>(__VA_ARGS__) : FN<SK_N, 2, false>(__VA_ARGS__);     \
-    case 4: return extras ? FN<SK_N, 4, true>(__VA_ARGS__) : FN<SK_N, 4, false>(__VA_ARGS__);     \
-    case 8: return extras ? FN<SK_N, 8, true>(__VA_ARGS__) : FN<SK_N, 8, false>(__VA_ARGS__);     \
-    case 16: return extras ? FN<SK_N, 16, true>(__VA_ARGS__) : FN<SK_N, 16, false>(__VA_ARGS__);  \
-    default: return cudaErrorInvalidValue;                                                        \
-  }
-#else
-#define SK_PAIR_SWITCH(FN, ...) return cudaErrorInvalidValue;
-#endif
-
 #define SK_CAT2(a, b) a##b
 #define SK_CAT(a, b) SK_CAT2(a, b)
 
@@ -155,16 +104,12 @@ static cudaError_t occupancy_pair(int* blocks_per_sm) {
     default: return cudaErrorInvalidValue;       \
   }
 
-cudaError_t SK_CAT(sweep_launch_n, SK_N)(int dp, bool exact, bool extras, bool paired, int grid, cudaStream_t stream,
+cudaError_t SK_CAT(sweep_launch_n, SK_N)(int dp, bool exact, bool extras, int grid, cudaStream_t stream,
                                          const SweepParams& P) {
-  if (paired && exact) return cudaErrorInvalidValue;
-  if (paired) SK_PAIR_SWITCH(launch_pair, grid, stream, P)
   SK_DP_SWITCH(launch_one, grid, stream, P)
 }
 
-cudaError_t SK_CAT(sweep_occupancy_n, SK_N)(int dp, bool exact, bool extras, bool paired, int* blocks_per_sm) {
-  if (paired && exact) return cudaErrorInvalidValue;
-  if (paired) SK_PAIR_SWITCH(occupancy_pair, blocks_per_sm)
+cudaError_t SK_CAT(sweep_occupancy_n, SK_N)(int dp, bool exact, bool extras, int* blocks_per_sm) {
   SK_DP_SWITCH(occupancy_one, blocks_per_sm)
 }
 

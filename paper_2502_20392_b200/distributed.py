@@ -48,12 +48,17 @@ def shard_mask(m: int, shard: int, nshards: int) -> np.ndarray:
 
 
 def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] = None, group=None,
-                            compute: Optional[Callable] = None, device=None) -> sk.GramResult:
+                            compute: Optional[Callable] = None, device=None, shard: int = 0,
+                            nshards: int = 1) -> sk.GramResult:
     """gram_matrix over all ranks of `group` (default: the world group).
 
-    `compute(family, options, shard, nshards) -> GramResult` evaluates one
-    shard; it defaults to the GPU path (sk.gram_matrix with shard/nshards).
-    Every rank returns the full assembled GramResult."""
+    The upper-triangle pairs of shard `shard` of `nshards` (default: the whole
+    Gram) are split over the ranks: rank r evaluates sub-shard
+    shard * world + r of nshards * world, so the ranks' ranges tile the shard
+    exactly.  `compute(family, options, shard, nshards) -> GramResult`
+    evaluates one sub-shard; it defaults to the GPU path (sk.gram_matrix).
+    Every rank returns the assembled GramResult (entries outside the shard
+    NaN, as gram_matrix leaves them)."""
     import torch
     import torch.distributed as dist
 
@@ -61,11 +66,15 @@ def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] 
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     compute = compute or (lambda fam, opt, s, n: sk.gram_matrix(fam, opt, shard=s, nshards=n))
-    fam = [sk._as_series(s) for s in family]
-    m = len(fam)
+    if isinstance(family, np.ndarray) and family.ndim == 3:
+        fam = family  # an (m, length, dim) block: gram_matrix's no-copy path
+        m, length = family.shape[0], max(2, family.shape[1])
+    else:
+        fam = [sk._as_series(s) for s in family]
+        m, length = len(fam), max(2, max(s.length() for s in fam))
     err = None
     try:
-        local = compute(fam, options, rank, world)
+        local = compute(fam, options, shard * world + rank, nshards * world)
     except sk.InconsistentBoundaryError as e:  # gram.cpp:74-77 lets it propagate
         err, local = str(e), None
     if device is None:
@@ -75,7 +84,7 @@ def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] 
     dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
     if flag.item() > 0:
         raise sk.InconsistentBoundaryError(err or "inconsistent boundary on another rank")
-    mask = shard_mask(m, rank, world)
+    mask = shard_mask(m, shard * world + rank, nshards * world)
     vals = np.where(mask, np.asarray(local.values).reshape(m, m), 0.0)
     ords = np.where(mask, np.asarray(local.orders).reshape(m, m), 0).astype(np.float64)
     pmax = np.zeros((m, m)) if local.pair_max_abs_rho is None else \
@@ -88,17 +97,20 @@ def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] 
     failures = [None] * world
     dist.all_gather_object(failures, [(f.row, f.col, f.message) for f in local.failures], group=group)
     out = buf.cpu().numpy()
+    if nshards > 1:
+        outside = ~shard_mask(m, shard, nshards)
+        out[0][outside] = np.nan
     r = sk.GramResult(size=m, values=out[0].ravel(), orders=out[1].ravel().astype(np.int32),
                       adaptive=local.adaptive, orders_converged=stats[1].item() == 0.0,
                       wall_seconds=local.wall_seconds)
     r.failures = [sk.GramEntryError(a, b, msg) for lst in failures for (a, b, msg) in lst]
     r.failures.sort(key=lambda e: (e.row, e.col))
-    r.min_order = int(r.orders.min())
-    r.max_order = int(r.orders.max())
+    computed = r.orders[r.orders > 0]
+    r.min_order = int(computed.min()) if computed.size else 0
+    r.max_order = int(computed.max()) if computed.size else 0
     r.max_abs_increment_product = float(stats[0].item())
     r.pair_max_abs_rho = out[2].ravel()
     n_ok = int(np.sum(~np.isnan(r.values)))
-    length = max(2, max(s.length() for s in fam))
     r.peak_live_series = sk._peak_live(length - 1, length - 1) if n_ok else 0
     if options.compute_bound:
         r.bound = sk.gram_error_bound(sk.ErrorBoundInputs(m, length, r.max_abs_increment_product, r.min_order))

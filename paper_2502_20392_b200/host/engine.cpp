@@ -163,27 +163,34 @@ GramResult gram_matrix(const std::vector<TimeSeries>& family, const GramOptions&
   r.adaptive = adaptive;
   r.values.assign(m * m, std::numeric_limits<double>::quiet_NaN());
   r.orders.assign(m * m, 0);
-  std::vector<sk_status> per(m * m);
   int conv = 1;
   double maxp = 0.0;
   sk_status st{};
   const uint32_t flags = (options.strict_corner ? SK_STRICT_CORNER : 0u) |
                          (tile::detail::w_fault_for_testing() ? SK_W_FAULT : 0u);
+  // the calling thread's failure records of its last sk_gram call (sparse)
+  auto take_failures = [](std::size_t n, std::vector<GramEntryError>& out) {
+    std::vector<sk_gram_failure> buf(n);
+    n = sk_gram_failures(buf.data(), n);
+    for (std::size_t k = 0; k < n; ++k) out.push_back({buf[k].row, buf[k].col, buf[k].status.message});
+  };
   const auto t0 = std::chrono::steady_clock::now();
   const std::size_t nd = options.devices.size();
   if (nd <= 1) {
     if (nd == 1) check(sk_set_device(options.devices[0], &st), st);
+    std::size_t nf = 0;
     check(sk_gram(buf.data(), m, max_len, dim, adaptive ? 1 : 0, options.policy.order, options.policy.tol, flags,
                   scan ? 1 : 0, options.shard, options.nshards, r.values.data(), r.orders.data(), nullptr, &maxp,
-                  &conv, per.data(), &st),
+                  &conv, &nf, &st),
           st);
+    take_failures(nf, r.failures);
   } else {
     // one host thread per device, each a sub-shard (shard * nd + k of nshards * nd);
     // every thread owns its context, so the calls run concurrently
     struct Part {
       std::vector<double> values;
       std::vector<int> orders;
-      std::vector<sk_status> per;
+      std::vector<GramEntryError> failures;
       double maxp = 0.0;
       int conv = 1;
       sk_status st{};
@@ -196,12 +203,13 @@ GramResult gram_matrix(const std::vector<TimeSeries>& family, const GramOptions&
         Part& pt = parts[k];
         pt.values.assign(m * m, 0.0);
         pt.orders.assign(m * m, 0);
-        pt.per.assign(m * m, sk_status{});
         pt.rc = sk_set_device(options.devices[k], &pt.st);
+        std::size_t nf = 0;
         if (pt.rc == SK_OK)
           pt.rc = sk_gram(buf.data(), m, max_len, dim, adaptive ? 1 : 0, options.policy.order, options.policy.tol,
                           flags, scan ? 1 : 0, options.shard * nd + k, options.nshards * nd, pt.values.data(),
-                          pt.orders.data(), nullptr, &pt.maxp, &pt.conv, pt.per.data(), &pt.st);
+                          pt.orders.data(), nullptr, &pt.maxp, &pt.conv, &nf, &pt.st);
+        if (pt.rc == SK_OK) take_failures(nf, pt.failures);
       });
     for (auto& t : pool) t.join();
     for (Part& pt : parts) check(pt.rc, pt.st);
@@ -217,20 +225,18 @@ GramResult gram_matrix(const std::vector<TimeSeries>& family, const GramOptions&
             for (const std::size_t e : {i * m + j, j * m + i}) {
               r.values[e] = parts[k].values[e];
               r.orders[e] = parts[k].orders[e];
-              per[e] = parts[k].per[e];
             }
             break;
           }
+    // sub-shards are consecutive row-major ranges: concatenation keeps the order
     for (const Part& pt : parts) {
       maxp = std::max(maxp, pt.maxp);
       conv = conv && pt.conv;
+      r.failures.insert(r.failures.end(), pt.failures.begin(), pt.failures.end());
     }
   }
   r.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   r.orders_converged = conv != 0;
-  for (std::size_t i = 0; i < m; ++i)
-    for (std::size_t j = i; j < m; ++j)
-      if (per[i * m + j].code != SK_OK) r.failures.push_back({i, j, per[i * m + j].message});
   int lo = std::numeric_limits<int>::max(), hi = 0;
   std::size_t ok = 0;
   for (std::size_t e = 0; e < m * m; ++e) {

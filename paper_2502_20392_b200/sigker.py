@@ -499,6 +499,15 @@ def _status_array(n: int) -> np.ndarray:
     return np.zeros(n, dtype=dt)
 
 
+def _gram_failures(lib, count: int) -> List[GramEntryError]:
+    """The calling thread's last sk_gram failure records (sparse, row-major)."""
+    if count == 0:
+        return []
+    buf = (_capi.SkGramFailure * count)()
+    n = lib.sk_gram_failures(buf, count)
+    return [GramEntryError(int(f.row), int(f.col), f.status.message.decode(errors="replace")) for f in buf[:n]]
+
+
 def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: int = 0,
                 nshards: int = 1) -> GramResult:
     """gram.hpp:46 (gram.cpp:16-98).  With nshards > 1 only this shard's
@@ -506,18 +515,33 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     partition of the multi-GPU Gram."""
     import time
     options = options or GramOptions()
-    fam = [_as_series(s) for s in family]
-    if not fam:
-        raise ValueError("gram_matrix: family must be nonempty")
-    dim = fam[0].dim()
-    max_len = 0
-    for s in fam:
-        if s.dim() != dim:
-            raise ValueError("gram_matrix: mixed dimensions in family")
-        max_len = max(max_len, s.length())
-    max_len = max(max_len, 2)
-    padded = np.stack([pad_to_length(s, max_len).values() for s in fam])
-    m = len(fam)
+    if isinstance(family, np.ndarray) and family.ndim == 3:
+        # an (m, length, dim) block is a family of equal-length series already
+        # padded (no per-series copies; one finiteness scan, time_series.cpp:9-19)
+        padded = np.ascontiguousarray(family, dtype=np.float64)
+        if padded.shape[0] == 0:
+            raise ValueError("gram_matrix: family must be nonempty")
+        if padded.shape[1] < 1 or padded.shape[2] < 1:
+            raise ValueError("time series must contain at least one point")
+        if not _capi.load().sk_all_finite(padded.ctypes.data, padded.size):
+            raise ValueError("time series coordinates must be finite")
+        m, max_len, dim = padded.shape
+        if max_len < 2:
+            padded = np.concatenate([padded, padded], axis=1)
+            max_len = 2
+    else:
+        fam = [_as_series(s) for s in family]
+        if not fam:
+            raise ValueError("gram_matrix: family must be nonempty")
+        dim = fam[0].dim()
+        max_len = 0
+        for s in fam:
+            if s.dim() != dim:
+                raise ValueError("gram_matrix: mixed dimensions in family")
+            max_len = max(max_len, s.length())
+        max_len = max(max_len, 2)
+        padded = np.stack([pad_to_length(s, max_len).values() for s in fam])
+        m = len(fam)
     adaptive = options.policy.mode == "adaptive"
     scan = adaptive or options.compute_bound
     lib = _capi.load()
@@ -527,23 +551,24 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     pmax = np.zeros(m * m)
     maxp = ctypes.c_double()
     conv = ctypes.c_int()
-    per = _status_array(m * m)
     flags = _capi.SK_STRICT_CORNER if options.strict_corner else 0
     if _W_FAULT[0]:
         flags |= _capi.SK_W_FAULT
     t0 = time.perf_counter()
 
-    def run_shard(sub, nsub, vals, ords, pm, mp, cv, pr, status):
-        return lib.sk_gram(_ptr(padded), m, max_len, dim, 1 if adaptive else 0, int(options.policy.order),
-                           float(options.policy.tol), flags, 1 if scan else 0, int(sub), int(nsub), _ptr(vals),
-                           _ptr(ords), _ptr(pm), ctypes.byref(mp), ctypes.byref(cv), _ptr(pr),
-                           ctypes.byref(status))
+    def run_shard(sub, nsub, vals, ords, pm, mp, cv, status):
+        nf = ctypes.c_size_t()
+        rc = lib.sk_gram(_ptr(padded), m, max_len, dim, 1 if adaptive else 0, int(options.policy.order),
+                         float(options.policy.tol), flags, 1 if scan else 0, int(sub), int(nsub), _ptr(vals),
+                         _ptr(ords), _ptr(pm), ctypes.byref(mp), ctypes.byref(cv), ctypes.byref(nf),
+                         ctypes.byref(status))
+        return rc, (_gram_failures(lib, nf.value) if rc == 0 else [])
 
     devices = list(options.devices)
     if len(devices) <= 1:
         if devices:
             _check(lib.sk_set_device(int(devices[0]), ctypes.byref(st)), st)
-        rc = run_shard(shard, nshards, values, orders, pmax, maxp, conv, per, st)
+        rc, failures = run_shard(shard, nshards, values, orders, pmax, maxp, conv, st)
         _check(rc, st)
     else:
         # one host thread per GPU (ctypes releases the GIL during the call);
@@ -551,15 +576,15 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
         import threading
         nd = len(devices)
         parts = [dict(values=np.zeros(m * m), orders=np.zeros(m * m, dtype=np.int32), pmax=np.zeros(m * m),
-                      maxp=ctypes.c_double(), conv=ctypes.c_int(), per=_status_array(m * m),
-                      st=_capi.SkStatus(), rc=0) for _ in range(nd)]
+                      maxp=ctypes.c_double(), conv=ctypes.c_int(), st=_capi.SkStatus(), rc=0, failures=[])
+                 for _ in range(nd)]
 
         def work(k):
             p = parts[k]
             p["rc"] = lib.sk_set_device(int(devices[k]), ctypes.byref(p["st"]))
             if p["rc"] == 0:
-                p["rc"] = run_shard(shard * nd + k, nshards * nd, p["values"], p["orders"], p["pmax"], p["maxp"],
-                                    p["conv"], p["per"], p["st"])
+                p["rc"], p["failures"] = run_shard(shard * nd + k, nshards * nd, p["values"], p["orders"], p["pmax"],
+                                                   p["maxp"], p["conv"], p["st"])
 
         threads = [threading.Thread(target=work, args=(k,)) for k in range(nd)]
         for t in threads:
@@ -582,17 +607,14 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
             values[sel] = p["values"][sel]
             orders[sel] = p["orders"][sel]
             pmax[sel] = p["pmax"][sel]
-            per[sel] = p["per"][sel]
+        # sub-shards are consecutive row-major ranges: concatenation keeps the order
+        failures = [f for p in parts for f in p["failures"]]
         maxp.value = max(p["maxp"].value for p in parts)
         conv.value = int(all(p["conv"].value for p in parts))
     wall = time.perf_counter() - t0
     r = GramResult(size=m, values=values, orders=orders, adaptive=adaptive, orders_converged=bool(conv.value),
                    wall_seconds=wall)
-    # failing upper-triangle entries in (i, j) row-major order
-    for e in np.flatnonzero(per["code"] != 0):
-        i, j = divmod(int(e), m)
-        if j >= i:
-            r.failures.append(GramEntryError(i, j, per["message"][e].decode(errors="replace")))
+    r.failures = failures
     computed = orders[orders > 0]
     r.min_order = int(computed.min()) if computed.size else 0
     r.max_order = int(computed.max()) if computed.size else 0
@@ -604,6 +626,57 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     if options.compute_bound:
         r.bound = gram_error_bound(ErrorBoundInputs(m, max_len, r.max_abs_increment_product, r.min_order))
     return r
+
+
+# ------------------------------------------------------------ input side
+_HOST_LIB = [None]
+
+
+def _host_lib():
+    """libsigker.so (the C++ drop-in library, host code) for datagen."""
+    if _HOST_LIB[0] is None:
+        import os
+        lib = ctypes.CDLL(os.path.join(os.path.dirname(_capi.LIB_PATH), "libsigker.so"))
+        lib.sigker_datagen_brownian.argtypes = [ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_void_p]
+        lib.sigker_datagen_brownian.restype = ctypes.c_int
+        _HOST_LIB[0] = lib
+    return _HOST_LIB[0]
+
+
+def brownian(length: int, dim: int, seed: int) -> np.ndarray:
+    """datagen.hpp brownian (datagen.cpp:78-88): the reference's value stream,
+    bit for bit (xoshiro256++ / splitmix64, polar Box-Muller)."""
+    out = np.empty((length, dim))
+    if _host_lib().sigker_datagen_brownian(length, dim, seed, out.ctypes.data) != 0:
+        raise ValueError("brownian: length must be >= 2 and dimension >= 1")
+    return out
+
+
+def brownian_family(length: int, dim: int, seeds: Sequence[int], out: Optional[np.ndarray] = None,
+                    threads: int = 8) -> np.ndarray:
+    """(len(seeds), length, dim) block of brownian(length, dim, seed) series,
+    generated by `threads` host threads (ctypes releases the GIL), into `out`
+    if given (e.g. a pinned buffer)."""
+    import threading
+    seeds = [int(s) for s in seeds]
+    if out is None:
+        out = np.empty((len(seeds), length, dim))
+    lib = _host_lib()
+    bad = []
+
+    def work(t):
+        for k in range(t, len(seeds), threads):
+            if lib.sigker_datagen_brownian(length, dim, seeds[k], out[k].ctypes.data) != 0:
+                bad.append(k)
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(max(1, threads))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if bad:
+        raise ValueError("brownian: length must be >= 2 and dimension >= 1")
+    return out
 
 
 # ---------------------------------------------------------------- helpers
@@ -629,4 +702,4 @@ def stats_get() -> dict:
     _capi.load().sk_stats_get(ctypes.byref(s))
     return {"sweep_launches": s.sweep_launches, "aux_launches": s.aux_launches, "sweep_ms": s.sweep_ms,
             "tiles": s.tiles, "tile_flops": s.tile_flops, "table_launches": s.table_launches,
-            "table_ms": s.table_ms, "paired_launches": s.paired_launches}
+            "table_ms": s.table_ms, "literal_rechecks": s.literal_rechecks}

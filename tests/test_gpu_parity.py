@@ -163,10 +163,15 @@ def test_error_contract(sk):
 
 
 def test_inconsistent_boundary_contract(sk, restatement):
-    """Scaled-volatility Brownian pairs on which the reference's corner check
-    fires (tile_series.cpp:70-75).  Strict mode follows the reference (the
-    exact tile may differ within rounding, so only the error type is pinned);
-    with the check off the value is the check-free restatement's."""
+    """Scaled-volatility Brownian pairs near the reference's corner check
+    (tile_series.cpp:70-75).  Strict mode (the C++ API default) must decide
+    exactly as the reference does: raise InconsistentBoundaryError where the
+    reference raises -- at the tile where the reference's sweep throws (the
+    restatement, bit-identical to the reference, locates it) -- and return the
+    reference's value where it returns one.  The register kernels screen the
+    corner at 1e-11 and hand screened pairs to the literal (bit-identical)
+    kernel, so a returned value is then the reference's bits.  With the check
+    off the value is the check-free restatement's."""
     for c in load("errors.json")["cases"]:
         if "recipe" not in c:
             continue
@@ -175,11 +180,49 @@ def test_inconsistent_boundary_contract(sk, restatement):
         r = sk.propagate(x, y, c["order"], loose)
         expect = c.get("checkfree_value", c.get("value"))
         assert rel(r.value, expect) < TOL, (c["name"], r.value, expect)
+        sk.stats_enable(True)
+        sk.stats_reset()
         if "code" in c:
-            try:
+            _, _, _, tile = restatement.propagate_probe(x, y, c["order"])
+            with pytest.raises(sk.InconsistentBoundaryError) as e:
                 sk.propagate(x, y, c["order"])
-            except sk.InconsistentBoundaryError:
-                pass
+            assert f"tile ({tile[0]}, {tile[1]})" in str(e.value), (c["name"], str(e.value), tile)
+            assert sk.stats_get()["literal_rechecks"] == 1
+        else:
+            v = sk.propagate(x, y, c["order"]).value
+            if sk.stats_get()["literal_rechecks"]:
+                assert v == c["value"], c["name"]
+            else:
+                assert rel(v, c["value"]) < TOL, c["name"]
+        sk.stats_enable(False)
+
+
+def test_strict_corner_screen_spares_clean_pairs(sk, restatement):
+    """Brownian inputs sit far below the 1e-11 screen: strict mode re-sweeps
+    nothing and equals the unchecked result bit for bit."""
+    xs = np.stack([restatement.brownian(700, 4, 70 + k) for k in range(6)])
+    ys = np.stack([restatement.brownian(650, 4, 80 + k) for k in range(6)])
+    sk.stats_enable(True)
+    sk.stats_reset()
+    strict = sk.pairwise(xs, ys, sk.TruncationPolicy.adaptive(1e-12))
+    assert sk.stats_get()["literal_rechecks"] == 0
+    sk.stats_enable(False)
+    loose = sk.pairwise(xs, ys, sk.TruncationPolicy.adaptive(1e-12), sk.PropagateOptions(strict_corner=False))
+    assert strict.values.tolist() == loose.values.tolist()
+
+
+def test_strict_corner_screen_in_batches_and_grams(sk, restatement):
+    """The literal re-sweep inside pairwise and gram: a throwing pair is a
+    per-pair InconsistentBoundaryError in pairwise (raised, as the reference
+    would on that pair) and aborts gram_matrix (gram.cpp:74-77 lets it
+    through); a screened pair that the reference accepts keeps its value."""
+    throw = load("errors.json")["cases"]
+    hot = [c for c in throw if c.get("name") == "sigma12.0"][0]
+    x, y = brown_pair(restatement, hot["recipe"])
+    with pytest.raises(sk.InconsistentBoundaryError):
+        sk.pairwise(np.stack([x, x]), np.stack([y, x]), sk.TruncationPolicy.adaptive(1e-12))
+    with pytest.raises(sk.InconsistentBoundaryError):
+        sk.gram_matrix([x, y], sk.GramOptions(policy=sk.TruncationPolicy.adaptive(1e-12)))
 
 
 def test_overflow_inside_batch_is_per_pair(sk, restatement):

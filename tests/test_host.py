@@ -35,7 +35,7 @@ def test_capi_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", _capi.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (sk_[a-z_0-9]+)$", out, re.M))
     assert set(declared) <= exported
-    assert lib.sk_abi_version() == 2
+    assert lib.sk_abi_version() == 3
 
 
 def test_estimate_order_matches_reference_table():
@@ -268,3 +268,47 @@ def test_long_pair_devices_rejects_a_shared_gpu():
     x = np.cumsum(np.ones((40, 2)), axis=0)
     with pytest.raises(ValueError, match="distinct"):
         skd.propagate_long_pair_devices(x, x, 8, devices=[0, 0])
+
+
+# ------------------------------------------------------------- bench plumbing
+def test_bench_step_ranges_tile_the_gram():
+    """bench.py's step split: for every world size the ranks' ranges tile
+    each slice, and the slices tile the upper triangle, in row-major order
+    (sk_gram_shard_range arithmetic)."""
+    import bench
+    for ws in (1, 2, 3, 8):
+        covered = []
+        for step in range(bench.SLICES):
+            parts = [bench.step_range(step, r, ws) for r in range(ws)]
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c
+            covered.append((parts[0][0], parts[-1][1]))
+        assert covered[0][0] == 0 and covered[-1][1] == bench.TOTAL_PAIRS
+        for (a, b), (c, d) in zip(covered, covered[1:]):
+            assert b == c
+    lib = __import__("paper_2502_20392_b200._capi", fromlist=["load"]).load()
+    import ctypes
+    lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
+    for shard, n in ((0, 32), (5, 64), (63, 64)):
+        lib.sk_gram_shard_range(bench.M, shard, n, ctypes.byref(lo), ctypes.byref(hi))
+        assert (lo.value, hi.value) == bench.pair_range(bench.TOTAL_PAIRS, shard, n)
+    assert bench.pair_of(0) == (0, 0) and bench.pair_of(bench.M) == (1, 1)
+    assert bench.pair_of(bench.TOTAL_PAIRS - 1) == (bench.M - 1, bench.M - 1)
+
+
+def test_bench_spawns_ranks_and_assembles_over_gloo():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under
+    torch.distributed.run; --cpu-smoke runs the multi-rank split, all-reduce
+    assembly and max-over-ranks timing over gloo with the C restatement as
+    the per-rank computation."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--cpu-smoke"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["world_size"] == 2 and line["assembled_equals_single_process"]
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64"], capture_output=True,
+                         text=True, timeout=300, cwd=ROOT)
+    assert out.returncode != 0 and "GPU(s) visible" in out.stderr
