@@ -191,8 +191,6 @@ typedef struct sk_stats {
   double sweep_ms;         /* summed device time of the sweep launches    */
   double tiles;            /* tile-updates processed by those launches    */
   double tile_flops;       /* algorithmic FP64 flops, sum of F(N,d) per tile */
-  uint64_t table_launches; /* rho-table builds (d > 16: DMMA GEMM)        */
-  double table_ms;         /* summed device time of those builds          */
   uint64_t literal_rechecks; /* strict corner: pairs re-swept with the literal kernel (ABI 3) */
 } sk_stats;
 

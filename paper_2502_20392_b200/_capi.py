@@ -47,8 +47,7 @@ class SkGramFailure(ctypes.Structure):
 class SkStats(ctypes.Structure):
     _fields_ = [("sweep_launches", ctypes.c_uint64), ("aux_launches", ctypes.c_uint64),
                 ("sweep_ms", ctypes.c_double), ("tiles", ctypes.c_double),
-                ("tile_flops", ctypes.c_double), ("table_launches", ctypes.c_uint64),
-                ("table_ms", ctypes.c_double), ("literal_rechecks", ctypes.c_uint64)]
+                ("tile_flops", ctypes.c_double), ("literal_rechecks", ctypes.c_uint64)]
 
 
 _lib = None

@@ -1,7 +1,7 @@
 // Auxiliary kernels around the sweep: increments (K1), the order pre-pass
 // (per-series increment norms for the Cauchy-Schwarz bound and the exact
-// max|rho| scan), the skewed rho table for large d, knot-grid boundary
-// initialisation and single-tile entry points.
+// max|rho| scan), knot-grid boundary initialisation, re-sweep bookkeeping and
+// single-tile entry points.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -160,8 +160,10 @@ __global__ void maxrho_scan_kernel(const double* __restrict__ xinc, const double
     atomicMax(out + pr, static_cast<unsigned long long>(__double_as_longlong(best)));
 }
 
-// rho table for the large-d path (d > 16): rho[i][j] = <dy_i, dx_j>, row-major
-// rows x cols per pair; the sweep gathers its deltas from it.
+// rho table for the large-d path (d > 16) when it fits the memory budget
+// (run_sweeps): rho[i][j] = <dy_i, dx_j>, row-major rows x cols per pair; the
+// sweep gathers its deltas from it.  Above the budget the sweep's producer
+// warps form rho in shared memory instead (sk_sweep.cuh, O(l) memory).
 //
 // Exact variant: sequential non-FMA dot (bit-identical deltas, needed when
 // the caller asks for the exact max|rho|).  One thread per entry.
@@ -189,11 +191,6 @@ constexpr int kGK = 32;            // k chunk
 constexpr int kGS = kGK + 4;       // smem row stride (doubles): conflict-free fragment loads
 constexpr int kGemmSmem = 2 * 2 * kGT * kGS * 8;
 
-__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
 
 __global__ void __launch_bounds__(128) rho_gemm_kernel(const double* __restrict__ xinc,
                                                        const double* __restrict__ yinc,

@@ -167,7 +167,6 @@ struct DevBuf {
 struct StatRec {
   cudaEvent_t a, b;
   double tiles, flops;
-  bool table;  // rho-table GEMM (large d) rather than a sweep
 };
 
 struct Ctx {
@@ -186,8 +185,8 @@ struct Ctx {
   size_t free_cache = 0;
   int free_age = 0;
   std::map<int, int> occupancy;
-  uint64_t sweep_launches = 0, aux_launches = 0, table_launches = 0, literal_rechecks = 0;
-  double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0, done_table_ms = 0.0;
+  uint64_t sweep_launches = 0, aux_launches = 0, literal_rechecks = 0;
+  double done_ms = 0.0, done_tiles = 0.0, done_flops = 0.0;
 
   // pinned staging for large pageable uploads (h2d): two buffers per worker
   std::vector<void*> stage;
@@ -202,7 +201,7 @@ struct Ctx {
       cudaEventDestroy(r.b);
     }
     DevBuf* all[] = {&raw_x, &raw_y, &xinc, &yinc, &sqn, &pairs, &values, &err, &maxr,
-                     &prog,  &queue, &abuf, &tab,  &grid, &diag, &w65,   &tile_io, &scan, &wd,
+                     &prog,  &queue, &abuf, &tab, &grid, &diag, &w65,   &tile_io, &scan, &wd,
                      &susp,  &dep,   &rq,   &redo, &redo_out, &gpairs};
     for (DevBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
@@ -366,6 +365,10 @@ int check_watchdog(Ctx& c, sk_status* st) {
   std::fprintf(stderr, "[sk] dependency waits: %.2f%% of band time (%.2f%% at band start)\n",
                h[7] ? 100.0 * h[6] / h[7] : 0.0, h[7] ? 100.0 * h[5] / h[7] : 0.0);
 #endif
+#ifdef SK_RHO_PROFILE
+  std::fprintf(stderr, "[sk] rho ring: consumer waited %.3f ms, producer waited %.3f ms, producer busy %.3f ms (summed over bands)\n",
+               h[5] * 1e-6, h[6] * 1e-6, h[7] * 1e-6);
+#endif
   if (h[0] == 0) return SK_OK;
   return set_status(st, SK_INTERNAL, 0, 0,
                     "sweep watchdog: dependency wait timed out (pair %llu band %llu needs %llu, saw %llu)", h[1], h[2],
@@ -422,7 +425,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // sequential one only where it could raise the exact max: they need a bound
   // on |fused - sequential| <= 2 d u sum|x_c y_c| <= 2 d u max||dx|| max||dy||
   double dot_err = 0.0;
-  if (exact && ntempl > 0 && dp > 0) {
+  if (exact && ntempl > 0) {
     const uint32_t nx = 1 + *std::max_element(px.begin(), px.end());
     const uint32_t ny = 1 + *std::max_element(py.begin(), py.end());
     SK_CUDA(c.sqn.ensure((nx + ny) * sizeof(double)));
@@ -437,13 +440,19 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     dot_err = 4.0 * ps.dim * std::ldexp(1.0, -53) * std::sqrt(mxx * mxy) * 1.01 + 1e-300;
   }
 
-  // large d: per-pair rho tables (rows x cols), pairs chunked to a memory budget
+  // Large d: a rho table per pair (rows x cols, one DMMA GEMM launch) when
+  // the tables of a launch fit a quarter of the free memory (at most 8 GB),
+  // else the band CTAs' producer warps form rho in shared memory -- O(l (N+d))
+  // memory whatever the length.  Measured on cfg 4 (l = 16384, d = 512): GEMM
+  // 8.7 ms + table sweep 19 ms vs fused 62 ms (the producers' L2 operand
+  // traffic, ~0.5 MB per band per 32 columns, slows the bands' hand-off
+  // chain), so the table wins where it fits.  SK_RHO_FUSED=1 forces fusion.
   const size_t tab_elems = dp == 0 ? static_cast<size_t>(rows) * cols : 0;
+  const size_t tab_budget = std::min<size_t>(free_b / 4, size_t(8) << 30);
+  const bool force_fused = std::getenv("SK_RHO_FUSED") != nullptr && std::getenv("SK_RHO_FUSED")[0] == '1';
+  const bool use_table = dp == 0 && !force_fused && tab_elems * sizeof(double) <= tab_budget;
   size_t chunk = npairs_all;
-  if (dp == 0) {
-    const size_t budget = std::max<size_t>(free_b / 3, tab_elems * sizeof(double));
-    chunk = std::max<size_t>(1, budget / (tab_elems * sizeof(double)));
-  }
+  if (use_table) chunk = std::max<size_t>(1, tab_budget / (tab_elems * sizeof(double)));
   // units per launch must fit 32 bits
   chunk = std::min<size_t>(chunk, std::max<size_t>(1, (size_t(1) << 31) / bands));
 
@@ -498,7 +507,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     const unsigned long long units = static_cast<unsigned long long>(npairs) * nb;
     int blocks = bps * c.sms;
     if (const char* e = std::getenv("SK_FORCE_BPS")) blocks = std::max(1, std::min(bps, std::atoi(e))) * c.sms;
-    const int per_block = kSweepWarps;
+    const int per_block = band_workers(ntempl, dp);  // bands swept concurrently per CTA
     const unsigned long long need_blocks = (units + per_block - 1) / per_block;
     if (static_cast<unsigned long long>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
     const size_t warps = static_cast<size_t>(blocks) * per_block;
@@ -553,18 +562,13 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
                               cudaMemcpyHostToDevice, c.stream()));
       SK_CUDA(cudaStreamSynchronize(c.stream()));  // `init` is pageable host memory
     }
-    if (dp == 0) {
+    if (use_table) {
       SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
-      // exact (sequential) deltas when max|rho| is reported or the literal
-      // (bit-identical) kernel runs; DMMA tensor-core GEMM otherwise
-      StatRec trec{};
-      trec.table = true;
-      if (int rc = record_start(c, &trec, st)) return rc;
+      // exact (sequential) deltas for the literal kernel, DMMA otherwise (the
+      // EXACT max|rho| re-forms candidates with the sequential dot)
       SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, ps.dim, ps.ld,
-                               exact || ntempl == 0, c.tab.as<double>(), tab_elems, c.stream()));
-      if (int rc = record_end(c, &trec, st)) return rc;
+                               ntempl == 0, c.tab.as<double>(), tab_elems, c.stream()));
       ++c.aux_launches;
-      ++c.table_launches;
     }
     SweepParams P{};
     P.xinc = ps.d_xinc;
@@ -575,9 +579,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.sx = ps.sx;
     P.sy = ps.sy;
     P.w65 = c.w65.as<double>() + ((flags & SK_W_FAULT) ? (kMaxOrder + 1) * (kMaxOrder + 1) : 0);
-    P.rho_tab = dp == 0 ? c.tab.as<double>() : nullptr;
-    P.tab_stride = tab_elems;
     P.dim = ps.dim;
+    P.ld = ps.ld;
+    P.rho_tab = use_table ? c.tab.as<double>() : nullptr;
+    P.tab_stride = tab_elems;
     P.order = order;
     P.rows = rows;
     P.cols = cols;
@@ -1595,8 +1600,8 @@ int sk_stats_reset(void) {
     cudaEventDestroy(r.b);
   }
   c->stats.clear();
-  c->sweep_launches = c->aux_launches = c->table_launches = c->literal_rechecks = 0;
-  c->done_ms = c->done_tiles = c->done_flops = c->done_table_ms = 0.0;
+  c->sweep_launches = c->aux_launches = c->literal_rechecks = 0;
+  c->done_ms = c->done_tiles = c->done_flops = 0.0;
   return SK_OK;
 }
 
@@ -1608,13 +1613,9 @@ int sk_stats_get(sk_stats* out) {
     cudaEventSynchronize(r.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
-    if (r.table) {
-      c->done_table_ms += ms;
-    } else {
-      c->done_ms += ms;
-      c->done_tiles += r.tiles;
-      c->done_flops += r.flops;
-    }
+    c->done_ms += ms;
+    c->done_tiles += r.tiles;
+    c->done_flops += r.flops;
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
@@ -1624,9 +1625,7 @@ int sk_stats_get(sk_stats* out) {
   out->sweep_ms = c->done_ms;
   out->tiles = c->done_tiles;
   out->tile_flops = c->done_flops;
-  out->table_launches = c->table_launches;
   out->literal_rechecks = c->literal_rechecks;
-  out->table_ms = c->done_table_ms;
   return SK_OK;
 }
 

@@ -75,6 +75,13 @@ __device__ __forceinline__ double exact_dot(const double (&a)[DP], const double 
   return acc;
 }
 
+// The same sequential dot over two rows in memory (large d; runtime length).
+__device__ __forceinline__ double exact_dot_rows(const double* a, const double* b, int dim) {
+  double acc = __dmul_rn(a[0], b[0]);
+  for (int c = 1; c < dim; ++c) acc = __dadd_rn(acc, __dmul_rn(a[c], b[c]));
+  return acc;
+}
+
 // 1/m as a compile-time-indexed constant (1 for m = 1, so no multiply).
 // Only these N+1 reciprocals appear as multipliers in the register solver:
 // few enough that ptxas keeps them in uniform registers, so every DFMA that
@@ -236,6 +243,15 @@ __device__ __forceinline__ double tile_step_literal(int order, const double* alp
     total = __dadd_rn(total, row_sum);
   }
   return total;
+}
+
+// FP64 tensor-core MMA (SASS DMMA): c[8x8] += a[8x4] b[4x8], one fragment
+// element per lane (a: row lane/4, k lane%4; b: k lane%4, column lane/4;
+// c: row lane/4, columns 2 (lane%4) + {0, 1}).
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {

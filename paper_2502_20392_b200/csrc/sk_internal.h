@@ -11,8 +11,8 @@ namespace skb {
 struct SweepParams;
 
 // Register-resident dot widths: d <= 16 is contracted inline in the sweep
-// (dy in registers, dx streamed through L1); larger d goes through the
-// skewed rho table (DP = 0).
+// (dy in registers, dx streamed through shared memory); larger d (DP = 0) is
+// contracted by the band CTA's producer warp on the FP64 tensor cores.
 inline int pick_dp(size_t dim) {
   if (dim <= 2) return 2;
   if (dim <= 4) return 4;
@@ -38,8 +38,8 @@ cudaError_t launch_max_sqnorm(const double* inc, size_t nseries, size_t count, s
 cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                                size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
                                int dim, int ld, unsigned long long* out, cudaStream_t st);
-// rho[i][j] tables (rows x cols, row-major) for the large-d path: DMMA GEMM,
-// or the bit-exact sequential dot when `exact`.
+// rho[i][j] tables (rows x cols, row-major) for the large-d path when they
+// fit the memory budget: DMMA GEMM, or the bit-exact sequential dot when `exact`.
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
                              int dim, int ld, bool exact, double* tab, unsigned long long tab_stride,

@@ -82,9 +82,13 @@ struct SweepParams {
   const uint32_t* pair_out;       // launch-local pair -> output slot
   unsigned long long sx, sy;      // elements between consecutive series
   const double* w65;              // N == 0: W table, row stride 65 (device memory)
-  const double* rho_tab;          // DP == 0: rho table (rows x cols, row-major) per launch-local pair
+  int dim, order;                 // dim: logical d
+  int ld;                         // row stride of the increments (DP, or d rounded up to 4 when DP == 0)
+  // DP == 0 table mode (the table fits the memory budget): rho (rows x cols,
+  // row-major) per launch-local pair, formed by the DMMA GEMM beforehand;
+  // null: the band CTAs' producer warps form rho in shared memory
+  const double* rho_tab;
   unsigned long long tab_stride;  // elements per pair in rho_tab
-  int dim, order;                 // dim: logical d (row stride of the increments is DP)
   int rows, cols, bands, npairs, group, slots;
   unsigned flags;
   double* abuf;                   // slots x cols x NP
@@ -179,7 +183,85 @@ __host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP) {
   return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + 32 * rows_per_lane(N) * col_stride(N) +
          (direct_top_out(DP) ? 0 : chunk_cols(rows_per_lane(N)) * col_stride(N)) +
          (DP > 0 ? ring_rows(rows_per_lane(N)) * ring_stride(DP) : 0) +
-         (DP > 0 ? 1 : 2) * rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32;
+         (DP > 0 ? rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32 : 0);
+}
+
+// ---- large d (DP == 0): the increment products are produced INSIDE the
+// sweep's CTA, never materialised in HBM.  Each band has a sweep warp (the
+// consumer) and a producer warp that computes the band's rho block by block
+// -- 32 rows x kRhoB columns, contracted over d with FP64 tensor-core MMA
+// (mma.sync m8n8k4, SASS DMMA), or with the reference's sequential non-FMA
+// dot for the literal kernel -- into a shared-memory ring of kRhoRB blocks
+// that the sweep warp reads at step s, lane t, column s - t.  Flow control:
+// two counters in shared memory (blocks produced, chunks consumed) with
+// CTA-scope release/acquire.  Memory per pair stays O(l (N+d)) whatever d
+// is (wavefront.cpp:100-105,146-149 form rho per tile too).
+#ifndef SK_RHO_KC
+#define SK_RHO_KC 16
+#endif
+#ifndef SK_RHO_STAGES
+#define SK_RHO_STAGES 3
+#endif
+constexpr int kRhoB = 32;                 // columns per produced block (4 MMA n-tiles)
+#ifndef SK_RHO_RB
+#define SK_RHO_RB 2
+#endif
+constexpr int kRhoRB = SK_RHO_RB;         // ring blocks
+constexpr int kRhoW = kRhoB * kRhoRB;     // ring columns (power of two)
+constexpr int kRhoKC = SK_RHO_KC;         // k (coordinate) chunk staged per cp.async group
+constexpr int kRhoKS = kRhoKC + 4;        // staging row stride: conflict-free fragment loads
+constexpr int kRhoStages = SK_RHO_STAGES; // cp.async pipeline depth
+static_assert((kRhoW & (kRhoW - 1)) == 0, "ring width must be a power of two");
+static_assert(kRhoW * 32 >= 2 * SK_CHUNK * 32, "table mode stages two chunks of deltas in the ring's memory");
+
+__host__ __device__ constexpr int rho_ring_doubles() { return kRhoW * 32; }
+__host__ __device__ constexpr int rho_stage_doubles() { return kRhoStages * (32 + kRhoB) * kRhoKS; }
+// DP == 0: one band's shared memory -- sweep stage | rho ring | producer staging
+__host__ __device__ constexpr int rho_slot_doubles(int N) {
+  return stage_doubles_per_warp(N, 0) + rho_ring_doubles() + rho_stage_doubles();
+}
+// A DP == 0 CTA sweeps rho_bands(N) bands (one CTA per SM): warps
+// 0..bands-1 are their sweep warps, the next `bands` warps their producers.
+// At most one sweep warp per SM sub-partition: warp w of a CTA runs on
+// sub-partition w mod 4, and two latency-bound sweep warps sharing one ran
+// ~2x slower (measured on cfg 4's sweep: one-warp band CTAs 19.3 ms vs
+// two-warp CTAs -- sweep warps on sub-partitions 0, 2, 0 -- 36.5 ms).  Four
+// bands when their shared memory fits the SM (N <= 13), fewer otherwise.
+constexpr int kSmemDoubles = 232448 / 8;  // 227 KB per CTA
+#ifndef SK_RHO_MAXBANDS
+#define SK_RHO_MAXBANDS 4
+#endif
+__host__ __device__ constexpr int rho_bands(int N) {
+  return kSmemDoubles / rho_slot_doubles(N) >= SK_RHO_MAXBANDS ? SK_RHO_MAXBANDS : kSmemDoubles / rho_slot_doubles(N);
+}
+__host__ __device__ constexpr int sweep_warps(int N, int DP) { return DP == 0 ? 2 * rho_bands(N) : kSweepWarps; }
+// bands swept concurrently by one CTA
+__host__ __device__ constexpr int band_workers(int N, int DP) { return DP == 0 ? rho_bands(N) : kSweepWarps; }
+// dynamic shared memory of one CTA (doubles)
+__host__ __device__ constexpr int sweep_smem_doubles(int N, int DP) {
+  return DP > 0 ? kSweepWarps * stage_doubles_per_warp(N, DP) : rho_bands(N) * rho_slot_doubles(N);
+}
+
+// producer / consumer hand-shake of a DP == 0 band CTA (static shared memory)
+struct RhoCtl {
+  unsigned p, b;        // the unit: pair (launch-local) and band
+  int c_begin, c_end;   // its chunk range
+  unsigned stop;        // no more units: producers exit
+  unsigned abort;       // the consumer abandoned the unit (watchdog)
+  unsigned prod;        // blocks < prod are in the ring (absolute block index)
+  unsigned cons;        // chunks < cons are done (absolute chunk index)
+};
+
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "r"(v) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(unsigned id, unsigned threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -315,7 +397,7 @@ __device__ __forceinline__ void sts_series(double* dst, const double (&v)[NA], i
 template <int N, int DP, bool EXACT, bool EXTRAS>
 __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsigned b, int lane,
                                           double* __restrict__ smem, int c_begin, int c_end, bool restore,
-                                          bool save) {
+                                          bool save, RhoCtl* ctl) {
   constexpr int R = rows_per_lane(N);
   constexpr int K = chunk_cols(R);
   constexpr int RING = ring_rows(R);
@@ -334,7 +416,13 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
   double* s_out = s_pass + 32 * R * NP;                     // K x NP
   double* s_ring = s_out + (direct_top_out(DP) ? 0 : kStage);  // RING x XS (DP > 0)
-  double* s_delta = s_ring + (DP > 0 ? RING * XS : 0);      // [buf][r][k][lane]
+  double* s_delta = s_ring + (DP > 0 ? RING * XS : 0);      // [r][k][lane] (DP > 0)
+  // DP == 0: the producers' rho ring, column c of row t at [(c mod kRhoW) * 32 + t];
+  // table mode: the same memory holds the staged table deltas [buf][k][lane]
+  const double* rho_ring = smem + stage_doubles_per_warp(N, 0);
+  const bool tab_mode = DP == 0 && P.rho_tab != nullptr;
+  double* s_tab = smem + stage_doubles_per_warp(N, 0);
+  const double* tab = DP > 0 || !tab_mode ? nullptr : P.rho_tab + static_cast<size_t>(p) * P.tab_stride;
   const int n = N > 0 ? N + 1 : P.order + 1;
   const int rows = P.rows, cols = P.cols;
   const int row0 = static_cast<int>(b) * 32 * R;
@@ -386,7 +474,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     yrow[r] = DP > 0 ? P.yinc + P.pair_y[p] * P.sy + static_cast<size_t>(row_ok[r] ? irow[r] + 1 : 0) * DP : nullptr;
   }
   const double* xser = DP > 0 ? P.xinc + P.pair_x[p] * P.sx + DP : nullptr;  // row j at xser + j * DP
-  const double* tab = DP > 0 ? nullptr : P.rho_tab + static_cast<size_t>(p) * P.tab_stride;  // rows x cols
+  // DP == 0: this pair's increments (exact dots of the EXACT candidates)
+  const double* xrows0 = DP > 0 ? nullptr : P.xinc + P.pair_x[p] * P.sx + P.ld;  // row j at xrows0 + j * ld
+  const double* yrows0 = DP > 0 ? nullptr : P.yinc + P.pair_y[p] * P.sy + P.ld;
 
   // Loop-carried register state: each tile's beta (the left edge of its next
   // tile), ping-ponged between A and B.  Before a tile's first column it runs
@@ -426,8 +516,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const int steps = cols + rb - 1;
 
   // ---- staging: group g = steps/columns [g K, g K + K): band-below alpha
-  // (2 buffers), dx (ring row = column mod RING) or, on the table path, the
-  // deltas of those steps (2 buffers); one cp.async group per g.
+  // (2 buffers) and dx (ring row = column mod RING; DP > 0) or the table
+  // deltas of those steps (DP == 0 table mode, 2 buffers); one cp.async group
+  // per g.
   auto stage_group = [&](int g) {
     const int col0 = g * K;
     const int ncol = max(0, min(K, cols - col0));
@@ -445,20 +536,17 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
         const int col = col0 + c;
         cp_async_16(s_ring + (col & (RING - 1)) * XS + 2 * part, xser + static_cast<size_t>(col) * DP + 2 * part);
       }
-    } else {
-      // row-major rho table: tile r of lane t gathers rho(i_r, g K + k - t - 32 r),
-      // zero-filled outside the pair (8-byte cp.async, consecutive lanes ->
-      // consecutive shared words)
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double* dst = s_delta + ((g & 1) * R + r) * K * 32 + lane;
-        const double* trow = tab + static_cast<size_t>(row_ok[r] ? irow[r] : 0) * cols;
+    } else if (tab_mode) {
+      // row-major table: lane t gathers rho(i, g K + k - t), zero-filled
+      // outside the pair (8-byte cp.async, consecutive lanes -> consecutive
+      // shared words)
+      double* dst = s_tab + (g & 1) * K * 32 + lane;
+      const double* trow = tab + static_cast<size_t>(row_ok[0] ? irow[0] : 0) * cols;
 #pragma unroll 4
-        for (int k = 0; k < K; ++k) {
-          const int j = col0 + k - lane - 32 * r;
-          const bool ok = row_ok[r] && j >= 0 && j < cols;
-          cp_async_8_zfill(dst + k * 32, trow + (ok ? j : 0), ok);
-        }
+      for (int k = 0; k < K; ++k) {
+        const int j = col0 + k - lane;
+        const bool ok = row_ok[0] && j >= 0 && j < cols;
+        cp_async_8_zfill(dst + k * 32, trow + (ok ? j : 0), ok);
       }
     }
     cp_async_commit();
@@ -537,8 +625,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
         jkey[r] = min(jkey[r], (act && !(fabs(delta) <= kDeltaOverflowLimit))
                                    ? (static_cast<unsigned>(j) << 2) | kErrDelta
                                    : ~0u);
-      } else {
+      } else if constexpr (DP > 0) {
         delta = dl[(r * K + k) * 32 + lane];
+      } else {
+        delta = tab_mode ? dl[k * 32 + lane] : rho_ring[((s - lane) & (kRhoW - 1)) * 32 + lane];
       }
       double qo[NA];
       double total = 0.0;
@@ -629,7 +719,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           }
         } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dd[u] = dl[(r * K + k0 + u) * 32 + lane];
+          for (int u = 0; u < 4; ++u)
+            dd[u] = tab_mode ? dl[(k0 + u) * 32 + lane] : rho_ring[((c0 + k0 + u - lane) & (kRhoW - 1)) * 32 + lane];
         }
         unsigned cand = 0u;  // EXACT, N > 0: tiles whose exact |delta| could raise the running max
 #pragma unroll
@@ -638,26 +729,33 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           const int j = c0 + k - lane - 32 * r;
           const bool act = row_ok[r] && j >= 0 && j < cols && k < kend;
           const double ad = fabs(dd[u]);
-          if constexpr (EXACT && (N == 0 || DP == 0)) mx = fmax(mx, act ? ad : 0.0);  // dd is exact here
-          if constexpr (EXACT && N > 0 && DP > 0) cand |= (act && ad + P.dot_err >= mx) ? 1u << u : 0u;
+          if constexpr (EXACT && N == 0) mx = fmax(mx, act ? ad : 0.0);  // dd is exact here
+          if constexpr (EXACT && N > 0) cand |= (act && ad + P.dot_err >= mx) ? 1u << u : 0u;
           const unsigned kk = (static_cast<unsigned>(j) << 2) | kErrDelta;
           jkey[r] = min(jkey[r], (act && !(ad <= kDeltaOverflowLimit)) ? kk : ~0u);
         }
-        if constexpr (EXACT && N > 0 && DP > 0) {
+        if constexpr (EXACT && N > 0) {
           // exact max|delta| (bit-identical to max_abs_rho) without an exact
-          // dot per tile: |fused - sequential| <= dot_err, so only a tile whose
-          // fused |delta| + dot_err reaches the running exact max can raise it
+          // dot per tile: |fast - sequential| <= dot_err, so only a tile whose
+          // fast |delta| + dot_err reaches the running exact max can raise it
           // -- rare once the max has settled; those get the sequential dot,
-          // re-reading their dx row from the ring
+          // re-reading their dx row from the ring (DP > 0) or both rows from
+          // global memory (DP == 0)
           if (__any_sync(0xffffffffu, cand != 0u)) {
 #pragma unroll 1
             for (int u = 0; u < 4; ++u)
               if ((cand >> u) & 1u) {
-                const double* xr = s_ring + ((c0 + k0 + u - lane - 32 * r) & (RING - 1)) * XS;
-                double row[DP];
+                if constexpr (DP > 0) {
+                  const double* xr = s_ring + ((c0 + k0 + u - lane - 32 * r) & (RING - 1)) * XS;
+                  double row[DP];
 #pragma unroll
-                for (int c = 0; c < DP; ++c) row[c] = xr[c];
-                mx = fmax(mx, fabs(exact_dot<DP>(row, dy)));
+                  for (int c = 0; c < DP; ++c) row[c] = xr[c];
+                  mx = fmax(mx, fabs(exact_dot<DP>(row, dy)));
+                } else {
+                  const int j = c0 + k0 + u - lane - 32 * r;
+                  mx = fmax(mx, fabs(exact_dot_rows(xrows0 + static_cast<size_t>(j) * P.ld,
+                                                    yrows0 + static_cast<size_t>(irow[r]) * P.ld, P.dim)));
+                }
               }
           }
         }
@@ -711,8 +809,41 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     }
     __syncwarp();
     const double* stage = s_alpha + (chunk & 1) * kStage;
-    const double* dl = s_delta + (DP > 0 ? 0 : (chunk & 1) * R * K * 32);
+    const double* dl = DP > 0 ? s_delta : s_tab + (chunk & 1) * K * 32;
     const int kend = min(K, steps - c0);
+    if (DP == 0 && !tab_mode) {
+      // the producers have written every column this chunk reads: < c0 + K
+      // (columns at or past `cols` belong to finished rows and are not used)
+      const unsigned need = static_cast<unsigned>((min(cols, c0 + K) + kRhoB - 1) / kRhoB);
+      int stuck = 0;
+      if (lane == 0 && ld_acquire_cta_u32(&ctl->prod) < need) {
+        const unsigned long long t0 = globaltimer_ns();
+#ifdef SK_RHO_PROFILE
+        struct Acc {
+          unsigned long long t0;
+          unsigned long long* dst;
+          __device__ ~Acc() { atomicAdd(dst, globaltimer_ns() - t0); }
+        } acc_wait{t0, P.watchdog + 5};
+#endif
+        unsigned ns = 16;
+        while (ld_acquire_cta_u32(&ctl->prod) < need) {
+          __nanosleep(ns);
+          if (ns < 256) ns *= 2;
+          if (globaltimer_ns() - t0 > P.watchdog_ns) {
+            if (atomicCAS(P.watchdog, 0ull, 1ull) == 0ull) {
+              P.watchdog[1] = p;
+              P.watchdog[2] = b;
+              P.watchdog[3] = need;
+              P.watchdog[4] = ctl->prod;
+            }
+            stuck = 1;
+            break;
+          }
+        }
+      }
+      if (__shfl_sync(0xffffffffu, stuck, 0)) return kBandAbort;
+      __syncwarp();  // lane 0's acquire before every lane reads the ring
+    }
     form_deltas(c0, kend, dl);
     __syncwarp();
     auto run_chunk = [&](bool tot) {
@@ -740,6 +871,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
         run_chunk(false);
     }
     hand_up(c0, kend);
+    if (DP == 0 && !tab_mode) {
+      __syncwarp();  // every lane's ring reads of this chunk are done
+      if (lane == 0) st_release_cta_u32(&ctl->cons, static_cast<unsigned>(chunk + 1));
+    }
   }
   if (streaming && !has_above && P.bands > 1) {
     // the last band publishes completion too: the slot's next pair (p + slots)
@@ -774,17 +909,209 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   return kBandDone;
 }
 
+// ---- rho producer of a DP == 0 band CTA (warp 1): per unit, the band's
+// rho for columns [c_lo, c_hi) in blocks of 32 rows x kRhoB columns.
+// DMMA: rho = dY dX^T on the FP64 tensor cores, k staged through a
+// kRhoStages-deep cp.async pipeline that runs on across block boundaries.
+// EXACT_RHO (literal kernel): the reference's sequential non-FMA dot
+// (wavefront.cpp:146-149), lane = row, so every delta is the reference's bits.
+template <bool EXACT_RHO>
+__device__ __forceinline__ void rho_producer(const SweepParams& P, double* __restrict__ ring,
+                                             double* __restrict__ stg, RhoCtl* ctl, int lane, unsigned bar_start,
+                                             unsigned bar_end) {
+  constexpr int K = chunk_cols(1);
+  constexpr int kStageSz = (32 + kRhoB) * kRhoKS;
+  const int ld = P.ld;
+  const int nk = (ld + kRhoKC - 1) / kRhoKC;
+  for (;;) {
+    named_bar_sync(bar_start, 64);  // the band's sweep warp published the unit (or stop)
+    if (ctl->stop) return;
+    const unsigned p = ctl->p, b = ctl->b;
+    const int c_begin = ctl->c_begin;
+    const long long c_end_cols = static_cast<long long>(ctl->c_end) * K;
+    const int rows = P.rows, cols = P.cols;
+    const int row0 = static_cast<int>(b) * 32;
+    const int c_lo = max(0, c_begin * K - 31);
+    const int c_hi = static_cast<int>(min(static_cast<long long>(cols), c_end_cols));
+    const int q0 = c_lo / kRhoB, q1 = (c_hi + kRhoB - 1) / kRhoB;
+    const int T = max(0, q1 - q0) * nk;
+    const double* xs = P.xinc + P.pair_x[p] * P.sx + ld;  // column j's increments at xs + j * ld
+    const double* ys = P.yinc + P.pair_y[p] * P.sy + ld;  // row i's at ys + i * ld
+    // columns before 0 read delta = 0 (a tile's unit-series steps before its
+    // first column); ring slots not yet produced are never read by live tiles
+    for (int e = lane; e < kRhoW * 32; e += 32) ring[e] = 0.0;
+    auto load = [&](int t) {
+      if (t < T) {
+        const int q = q0 + t / nk, k0 = (t - (t / nk) * nk) * kRhoKC;
+        double* A = stg + (t % kRhoStages) * kStageSz;
+        for (int e = lane; e < (32 + kRhoB) * (kRhoKC / 2); e += 32) {
+          const int r = e / (kRhoKC / 2), c = (e - r * (kRhoKC / 2)) * 2;
+          const int k = k0 + c;
+          const bool is_a = r < 32;
+          const int idx = is_a ? row0 + r : q * kRhoB + (r - 32);
+          const bool ok = (is_a ? idx < rows : idx < cols) && k < ld;
+          const double* src = (is_a ? ys : xs) + static_cast<size_t>(ok ? idx : 0) * ld + (ok ? k : 0);
+          cp_async_16_zfill(A + r * kRhoKS + c, src, ok);
+        }
+      }
+      cp_async_commit();
+    };
+#ifdef SK_RHO_PROFILE
+    const unsigned long long tu = globaltimer_ns();
+#endif
+#pragma unroll
+    for (int t = 0; t < kRhoStages - 1; ++t) load(t);
+    double acc[EXACT_RHO ? 32 : 4 * 4 * 2];
+#pragma unroll
+    for (int e = 0; e < (EXACT_RHO ? 32 : 32); ++e) acc[e] = 0.0;
+    bool aborted = false;
+    for (int t = 0; t < T; ++t) {
+      cp_async_wait<kRhoStages - 2>();
+      __syncwarp();
+      const double* A = stg + (t % kRhoStages) * kStageSz;
+      const double* Bm = A + 32 * kRhoKS;
+      if constexpr (EXACT_RHO) {
+        // lane = row; 32 sequential dots, one per column of the block
+#pragma unroll 1
+        for (int k = 0; k < kRhoKC; ++k) {
+          const double av = A[lane * kRhoKS + k];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(av, Bm[c * kRhoKS + k]));
+        }
+      } else {
+#pragma unroll
+        for (int k4 = 0; k4 < kRhoKC; k4 += 4) {
+          double a[4], bb[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            a[m] = A[(m * 8 + (lane >> 2)) * kRhoKS + k4 + (lane & 3)];
+            bb[m] = Bm[(m * 8 + (lane >> 2)) * kRhoKS + k4 + (lane & 3)];
+          }
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              double (&c2)[2] = *reinterpret_cast<double (*)[2]>(&acc[(mt * 4 + nt) * 2]);
+              dmma_884(c2, a[mt], bb[nt]);
+            }
+        }
+      }
+      __syncwarp();  // the stage is read before it is refilled
+      load(t + kRhoStages - 1);
+      if (t - (t / nk) * nk == nk - 1) {
+        // block q done: wait until the consumer has left the ring slot
+        // (columns < (q - RB + 1) B are last read at step column + 31)
+        const int q = q0 + t / nk;
+        const long long need = static_cast<long long>(q - kRhoRB + 1) * kRhoB + 31;
+        int stop = 0;
+        if (lane == 0) {
+          unsigned ns = 32;
+#ifdef SK_RHO_PROFILE
+          const unsigned long long tw = globaltimer_ns();
+#endif
+          while (static_cast<long long>(ld_acquire_cta_u32(&ctl->cons)) * K < need) {
+            if (*reinterpret_cast<volatile unsigned*>(&ctl->abort)) {
+              stop = 1;
+              break;
+            }
+            __nanosleep(ns);
+            if (ns < 512) ns *= 2;
+          }
+#ifdef SK_RHO_PROFILE
+          atomicAdd(P.watchdog + 6, globaltimer_ns() - tw);
+#endif
+        }
+        if (__shfl_sync(0xffffffffu, stop, 0)) {
+          aborted = true;
+          break;
+        }
+        __syncwarp();
+        const int cbase = q * kRhoB;
+        if constexpr (EXACT_RHO) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            ring[((cbase + c) & (kRhoW - 1)) * 32 + lane] = acc[c];
+            acc[c] = 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int row = mt * 8 + (lane >> 2), col = nt * 8 + 2 * (lane & 3) + e;
+                ring[((cbase + col) & (kRhoW - 1)) * 32 + row] = acc[(mt * 4 + nt) * 2 + e];
+                acc[(mt * 4 + nt) * 2 + e] = 0.0;
+              }
+        }
+        __syncwarp();  // every lane's ring stores before lane 0 publishes them
+        if (lane == 0) st_release_cta_u32(&ctl->prod, static_cast<unsigned>(q + 1));
+      }
+    }
+    (void)aborted;
+#ifdef SK_RHO_PROFILE
+    if (lane == 0) atomicAdd(P.watchdog + 7, globaltimer_ns() - tu);
+#endif
+    cp_async_wait<0>();
+    __syncwarp();
+    named_bar_sync(bar_end, 64);  // the sweep warp finished the unit
+  }
+}
+
 // Persistent: grid = resident CTAs; dynamic shared memory =
-// kSweepWarps * stage_doubles_per_warp(N, DP) doubles.
+// sweep_smem_doubles(N, DP) doubles.  DP == 0: warps 0..B-1 sweep B bands,
+// warps B..2B-1 produce their rho (band slot k: sweep warp k, producer warp
+// B + k, named barriers 1 + 2k / 2 + 2k), B = rho_bands(N).
 template <int N, int DP, bool EXACT, bool EXTRAS>
-__global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_kernel(const SweepParams P) {
+__global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 ? 1 : sweep_min_blocks(N))
+    sweep_kernel(const SweepParams P) {
+  constexpr int kBands = DP == 0 ? rho_bands(N) : 1;
+  static_assert(DP > 0 || kBands >= 1, "a band's shared memory must fit the SM");
   extern __shared__ __align__(16) double s_dyn[];
-  double* smem = s_dyn + (threadIdx.x >> 5) * stage_doubles_per_warp(N, DP);
+  __shared__ RhoCtl s_ctls[kBands];
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int kslot = DP == 0 ? warp % kBands : 0;
+  RhoCtl& s_ctl = s_ctls[kslot];
+  const unsigned bar_start = 1u + 2u * kslot, bar_end = 2u + 2u * kslot;
+  double* smem = DP == 0 ? s_dyn + kslot * rho_slot_doubles(N) : s_dyn + warp * stage_doubles_per_warp(N, DP);
+  if constexpr (DP == 0) {
+    if (warp >= kBands) {
+      if (P.rho_tab != nullptr) return;  // table mode: no producers
+      double* ring = smem + stage_doubles_per_warp(N, 0);
+      rho_producer<N == 0>(P, ring, ring + rho_ring_doubles(), &s_ctl, lane, bar_start, bar_end);
+      return;
+    }
+  }
   constexpr int H = 32 * rows_per_lane(N);
   constexpr int K = chunk_cols(rows_per_lane(N));
   const unsigned nb = static_cast<unsigned>(P.band_end - P.band_begin);
   const unsigned gsz = static_cast<unsigned>(P.group) * nb;
+  // one unit; DP == 0: hand it to the producer warp first, and meet it again
+  // at the end (the ring is reused by the next unit)
+  const bool with_producer = DP == 0 && P.rho_tab == nullptr;
+  auto run_unit = [&](unsigned p, unsigned b, int c_begin, int c_end, bool restore, bool save) {
+    if (with_producer) {
+      if (lane == 0) {
+        s_ctl.p = p;
+        s_ctl.b = b;
+        s_ctl.c_begin = c_begin;
+        s_ctl.c_end = c_end;
+        s_ctl.stop = 0u;
+        s_ctl.abort = 0u;
+        s_ctl.prod = static_cast<unsigned>(max(0, c_begin * K - 31) / kRhoB);
+        s_ctl.cons = static_cast<unsigned>(c_begin);
+      }
+      named_bar_sync(bar_start, 64);
+    }
+    const int st = sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem, c_begin, c_end, restore, save, &s_ctl);
+    if (with_producer) {
+      if (st == kBandAbort && lane == 0) *reinterpret_cast<volatile unsigned*>(&s_ctl.abort) = 1u;
+      named_bar_sync(bar_end, 64);
+    }
+    return st;
+  };
   for (;;) {
     unsigned p, b;
     int c_begin = 0, c_end = 0x7fffffff, seg = 0;
@@ -795,8 +1122,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
       unsigned u = 0;
       if (lane == 0) u = atomicAdd(P.queue, 1u);
       u = __shfl_sync(0xffffffffu, u, 0);
-      if (u >= static_cast<unsigned>(P.npairs) * nb) return;
-      if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) return;
+      if (u >= static_cast<unsigned>(P.npairs) * nb) break;
+      if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) break;
       const unsigned g = u / gsz;
       const unsigned rem = u - g * gsz;
       const unsigned g0 = g * static_cast<unsigned>(P.group);
@@ -838,7 +1165,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
         }
       }
       u = __shfl_sync(0xffffffffu, u, 0);
-      if (u == ~0u) return;
+      if (u == ~0u) break;
       __syncwarp();  // lane 0's acquire of the unit before every lane reads its inputs
       const unsigned spb = static_cast<unsigned>(P.segs_per_band);
       const unsigned pb = u / spb;
@@ -857,7 +1184,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
     const unsigned long long gt0 = globaltimer_ns();
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (lane == 0) g_wwait[wid] = 0;
-    const int st = sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem, c_begin, c_end, restore, save);
+    const int st = run_unit(p, b, c_begin, c_end, restore, save);
     if (lane == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(P.watchdog + 7), clock64() - t0);
       const unsigned t = atomicAdd(&g_tidx, 1u);
@@ -873,9 +1200,9 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
       }
     }
 #else
-    const int st = sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem, c_begin, c_end, restore, save);
+    const int st = run_unit(p, b, c_begin, c_end, restore, save);
 #endif
-    if (st == kBandAbort) return;
+    if (st == kBandAbort) break;
     if (P.seg_cols > 0) {
       __syncwarp();  // every lane's outputs before lane 0 releases them
       if (lane == 0) {
@@ -913,6 +1240,10 @@ __global__ void __launch_bounds__(kSweepWarps * 32, sweep_min_blocks(N)) sweep_k
         atomicAdd(P.ctr + 2 * kCtrLine, 1u);
       }
     }
+  }
+  if (with_producer) {
+    if (lane == 0) s_ctl.stop = 1u;
+    named_bar_sync(bar_start, 64);  // releases the band slot's producer
   }
 }
 

@@ -17,7 +17,7 @@ namespace skb {
 
 template <int N, int DP, bool EXACT, bool EXTRAS>
 static size_t smem_bytes() {
-  return static_cast<size_t>(kSweepWarps) * stage_doubles_per_warp(N, DP) * sizeof(double);
+  return static_cast<size_t>(sweep_smem_doubles(N, DP)) * sizeof(double);
 }
 
 template <int N, int DP, bool EXACT, bool EXTRAS>
@@ -57,7 +57,7 @@ static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& 
     cudaMemsetAsync(tp, 0, kTraceUnits * 4 * sizeof(unsigned long long), stream);
   }
 #endif
-  sweep_kernel<N, DP, EXACT, EXTRAS><<<grid, kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>(), stream>>>(P);
+  sweep_kernel<N, DP, EXACT, EXTRAS><<<grid, sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS>(), stream>>>(P);
 #ifdef SK_PROFILE_WAITS
   if (const char* path = std::getenv("SK_UTRACE")) {
     static std::vector<unsigned long long> h(kTraceUnits * 4);
@@ -77,7 +77,7 @@ static cudaError_t occupancy_one(int* blocks_per_sm) {
   cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<N, DP, EXACT, EXTRAS>,
-                                                       kSweepWarps * 32, smem_bytes<N, DP, EXACT, EXTRAS>());
+                                                       sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS>());
 }
 
 #define SK_CAT2(a, b) a##b

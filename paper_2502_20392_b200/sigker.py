@@ -701,5 +701,4 @@ def stats_get() -> dict:
     s = _capi.SkStats()
     _capi.load().sk_stats_get(ctypes.byref(s))
     return {"sweep_launches": s.sweep_launches, "aux_launches": s.aux_launches, "sweep_ms": s.sweep_ms,
-            "tiles": s.tiles, "tile_flops": s.tile_flops, "table_launches": s.table_launches,
-            "table_ms": s.table_ms, "literal_rechecks": s.literal_rechecks}
+            "tiles": s.tiles, "tile_flops": s.tile_flops, "literal_rechecks": s.literal_rechecks}

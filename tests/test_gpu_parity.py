@@ -597,3 +597,43 @@ def test_grid_against_finite_differences(sk, restatement):
     s = sk.propagate_grid(x, x, 24)
     S = np.asarray(s.grid).reshape(s.grid_rows, s.grid_cols)
     assert np.max(np.abs(S - S.T)) < 1e-12
+
+
+def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
+    """d > 16: the rho table (GEMM into HBM, used where it fits the memory
+    budget) and the fused producer warps (rho formed in shared memory, O(l)
+    memory) run the same DMMA k-order or the same sequential dot, so every
+    output is bit-identical -- values, orders, max|rho|, knot grids, literal
+    orders, error tiles, strict-corner decisions; both against the oracle."""
+    rng = restatement.rng(4242)
+
+    def bits(v):
+        return np.ascontiguousarray(v, dtype=np.float64).view(np.int64).tolist()
+
+    x1, y1 = restatement.brownian(300, 40, 7), restatement.brownian(260, 40, 8)
+    xs = np.stack([rng.random_series(90, 33, 1.0) for _ in range(5)])
+    ys = np.stack([rng.random_series(150, 33, 1.0) for _ in range(5)])
+    xo = rng.random_series(70, 20, 1.0)
+    yo = rng.random_series(80, 20, 1.0)
+    xo[35:] *= 8e3
+    yo[40:] *= 8e3
+
+    def run_all():
+        out = [bits([sk.propagate(x1, y1, 8).value]), bits([sk.propagate(x1, y1, 20).value])]
+        a = sk.pairwise(xs, ys, sk.TruncationPolicy.adaptive(1e-12), want_max_abs_rho=True)
+        out.append((bits(a.values), list(a.orders), bits(a.max_abs_rho)))
+        out.append(bits(sk.propagate_grid(xs[0], ys[0], 8).grid))
+        try:
+            out.append(bits([sk.propagate(xo, yo, 8).value]))
+        except sk.NumericOverflowError as e:
+            out.append(("overflow", e.tile_k, e.tile_l))
+        return out
+
+    monkeypatch.setenv("SK_RHO_FUSED", "0")
+    table = run_all()
+    monkeypatch.setenv("SK_RHO_FUSED", "1")
+    fused = run_all()
+    assert fused == table
+    v_ref, _ = restatement.propagate(x1, y1, 20)
+    assert sk.propagate(x1, y1, 20).value == v_ref
+    assert rel(sk.propagate(x1, y1, 8).value, restatement.propagate(x1, y1, 8)[0]) < TOL

@@ -69,9 +69,7 @@ def main():
             x, y = brownian(1, 16384, 512, 1)[0], brownian(1, 16384, 512, 2)[0]
             sk.propagate_with_policy(x, y, pol, sk.PropagateOptions(strict_corner=False))
             r, wall, s = timed(lambda: sk.propagate_with_policy(x, y, pol, sk.PropagateOptions(strict_corner=False)))
-            gemm_tf = 2.0 * 16383 ** 2 * 512 / (s["table_ms"] / 1e3) / 1e12 if s["table_ms"] else 0.0
-            report("cfg4 l=16384 d=512", 16383 ** 2, wall, s,
-                   f"K={r.value!r} N={r.order}; rho GEMM {s['table_ms']:.2f} ms = {gemm_tf:.2f} TF/s")
+            report("cfg4 l=16384 d=512", 16383 ** 2, wall, s, f"K={r.value!r} N={r.order} (rho fused in the sweep)")
         elif cfg == "cfg5":
             m = a.m5
             fam = list(brownian(m, 4096, 16, 1000))
