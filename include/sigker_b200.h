@@ -156,16 +156,25 @@ int sk_gram_shard_range(size_t m, size_t shard, size_t nshards, size_t* first, s
  * split over host threads for large inputs.  Host memory, host work only. */
 int sk_all_finite(const double* v, size_t n);
 
-/* ---- Multi-GPU long pair: strip pipeline (cfg 3).
- * The ly-1 tile rows are cut into bands of 32*R rows (sk_strip_bands); GPU g
- * sweeps a contiguous band range and hands its top band's alpha series to
- * GPU g+1 through an exchange buffer in GPU g+1's memory (peer stores over
- * NVLink, system-scope release / acquire on a progress counter).  Setup: the
- * consumer allocates (sk_exchange_alloc) and exports (sk_ipc_handle) its
- * buffer; the producer maps it (sk_ipc_open).  All strips run concurrently. */
+/* ---- Multi-GPU long pair: block-cyclic strips (cfg 3).
+ * The ly-1 tile rows are cut into 32-row bands (sk_strip_bands), the bands
+ * into blocks of `block` bands, and the blocks are dealt round-robin over the
+ * GPUs: GPU g sweeps blocks g, g+G, g+2G, ... (rounds r = 0, 1, ...), all in
+ * one persistent launch.  At every block boundary the top band of block k
+ * streams its alpha series into the exchange area of the GPU of block k+1
+ * (peer stores over NVLink, system-scope release / acquire on a progress
+ * counter; GPU G-1 hands to GPU 0).  Contiguous strips (round 1) starve: a
+ * GPU's top band starts only after its whole strip has swept twice
+ * (tools/strip_sim.py).  Setup: every GPU allocates its exchange area with
+ * in_rounds of sk_strip_plan (sk_exchange_alloc) and exports it
+ * (sk_ipc_handle); the previous GPU maps it (sk_ipc_open).  All GPUs of the
+ * pair run concurrently.  Exchange areas hold `rounds` slots of (lx-1) x
+ * (order+1, even) doubles and `rounds` progress counters (128 B apart). */
 int sk_strip_bands(size_t ly, int order, size_t* bands);
-int sk_exchange_alloc(size_t lx, int order, void** abuf, void** prog, sk_status* st);
-int sk_exchange_reset(void* prog, sk_status* st);
+int sk_strip_plan(size_t ly, int order, size_t gpus, size_t rank, size_t block, size_t* owned_bands,
+                  size_t* rounds, size_t* in_rounds);
+int sk_exchange_alloc(size_t lx, int order, size_t rounds, void** abuf, void** prog, sk_status* st);
+int sk_exchange_reset(void* prog, size_t rounds, sk_status* st);
 int sk_exchange_free(void* abuf, void* prog);
 int sk_ipc_handle(void* dptr, void* handle64, sk_status* st);
 int sk_ipc_open(const void* handle64, void** dptr, sk_status* st);
@@ -174,14 +183,14 @@ int sk_ipc_close(void* dptr);
  * access `peer`'s memory, then pass exchange buffers as plain pointers. */
 int sk_enable_peer_access(int peer, sk_status* st);
 int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
-                       uint32_t flags, size_t band_begin, size_t band_end, const void* in_abuf,
+                       uint32_t flags, size_t gpus, size_t rank, size_t block, const void* in_abuf,
                        const void* in_prog, void* out_abuf, void* out_prog, double* value, double* diag,
                        sk_status* st);
-/* One-GPU emulation of a two-strip pipeline (single launch; the hand-off from
- * band split_band-1 to split_band goes through an exchange buffer with the
- * multi-GPU protocol).  Test entry point. */
+/* One-GPU emulation of the whole pipeline in a single launch: every `block`
+ * bands the hand-off goes through an exchange area with the multi-GPU
+ * protocol.  Test entry point. */
 int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
-                       uint32_t flags, size_t split_band, double* value, sk_status* st);
+                       uint32_t flags, size_t block, double* value, sk_status* st);
 
 /* Device-time accounting of the sweep kernels on the calling thread
  * (CUDA events around every sweep launch). */

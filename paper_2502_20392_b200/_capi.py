@@ -30,7 +30,7 @@ EXPORTED = [
     "sk_step_tile_fast", "sk_pairwise", "sk_pairwise_device", "sk_gram", "sk_gram_device", "sk_gram_failures",
     "sk_gram_shard_range", "sk_all_finite",
     "sk_stats_enable", "sk_stats_reset", "sk_stats_get", "sk_release",
-    "sk_strip_bands", "sk_exchange_alloc", "sk_exchange_reset", "sk_exchange_free", "sk_ipc_handle",
+    "sk_strip_bands", "sk_strip_plan", "sk_exchange_alloc", "sk_exchange_reset", "sk_exchange_free", "sk_ipc_handle",
     "sk_ipc_open", "sk_ipc_close", "sk_enable_peer_access", "sk_propagate_strip", "sk_propagate_split",
 ]
 
@@ -95,14 +95,15 @@ def load():
         "sk_stats_get": ([ctypes.POINTER(SkStats)], ctypes.c_int),
         "sk_release": ([], ctypes.c_int),
         "sk_strip_bands": ([SZ, ctypes.c_int, P], ctypes.c_int),
-        "sk_exchange_alloc": ([SZ, ctypes.c_int, P, P, ST], ctypes.c_int),
-        "sk_exchange_reset": ([P, ST], ctypes.c_int),
+        "sk_strip_plan": ([SZ, ctypes.c_int, SZ, SZ, SZ, P, P, P], ctypes.c_int),
+        "sk_exchange_alloc": ([SZ, ctypes.c_int, SZ, P, P, ST], ctypes.c_int),
+        "sk_exchange_reset": ([P, SZ, ST], ctypes.c_int),
         "sk_exchange_free": ([P, P], ctypes.c_int),
         "sk_ipc_handle": ([P, P, ST], ctypes.c_int),
         "sk_ipc_open": ([P, P, ST], ctypes.c_int),
         "sk_ipc_close": ([P], ctypes.c_int),
         "sk_enable_peer_access": ([ctypes.c_int, ST], ctypes.c_int),
-        "sk_propagate_strip": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, SZ, P, P, P, P, P, P, ST],
+        "sk_propagate_strip": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, SZ, SZ, P, P, P, P, P, P, ST],
                                ctypes.c_int),
         "sk_propagate_split": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, P, ST], ctypes.c_int),
     }

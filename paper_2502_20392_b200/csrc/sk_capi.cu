@@ -375,16 +375,35 @@ int check_watchdog(Ctx& c, sk_status* st) {
                     h[3], h[4]);
 }
 
-// A band range of one pair plus its cross-strip hand-off (multi-GPU long
-// pair, SweepParams::xin_* / xout_*).  Default: every band, no hand-off.
+// Long pair over several GPUs (SweepParams::xgpus ...): this GPU's share of
+// the block-cyclic band layout and the exchange areas of its block
+// boundaries.  Default: every band, one GPU, no hand-off.
 struct Strip {
-  int band_begin = 0, band_end = -1;
-  int xin_band = -1, xout_band = -1;
+  int gpus = 1, rank = 0, block = 0;  // block = 0: all bands in one block
+  bool exch = false;
   const double* xin_abuf = nullptr;
   const unsigned long long* xin_prog = nullptr;
   double* xout_abuf = nullptr;
   unsigned long long* xout_prog = nullptr;
 };
+
+// Block-cyclic strip plan: blocks k = 0 .. nblocks-1 of `block` bands; GPU g
+// owns k = g, g + G, ... (round r = k / G).  Returns the bands and rounds
+// (column buffers) GPU `rank` sweeps and the exchange rounds it receives
+// (blocks k >= 1 it owns: their bottom band's alpha comes from GPU k - 1).
+struct StripPlan {
+  size_t owned_bands = 0, rounds = 0, in_rounds = 0;
+};
+StripPlan strip_plan(size_t bands, size_t gpus, size_t rank, size_t block) {
+  StripPlan pl;
+  const size_t nblocks = (bands + block - 1) / block;
+  for (size_t k = rank; k < nblocks; k += gpus) {
+    pl.owned_bands += std::min(block, bands - k * block);
+    pl.rounds = k / gpus + 1;
+    if (k >= 1) pl.in_rounds = k / gpus + 1;
+  }
+  return pl;
+}
 
 // One persistent sweep launch per (order, pair chunk).  px/py/pout are
 // launch-local pair lists of equal length.
@@ -464,7 +483,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // (critical path under half the work, else under the work) is used;
   // otherwise the streaming schedule (a latency-bound short pair, multi-GPU
   // strips).
-  const bool whole = strip.band_begin == 0 && strip.band_end < 0 && strip.xin_band < 0 && strip.xout_band < 0;
+  const bool whole = strip.gpus == 1 && !strip.exch;
+  const size_t sblock = strip.block > 0 ? static_cast<size_t>(strip.block) : static_cast<size_t>(bands);
+  const StripPlan plan = strip_plan(static_cast<size_t>(bands), static_cast<size_t>(strip.gpus),
+                                    static_cast<size_t>(strip.rank), sblock);
   int seg_cols = 0;
   unsigned spb = 0, units_pair = 0;
   if (bands > 1 && whole && std::getenv("SK_STREAM") == nullptr) {
@@ -503,7 +525,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
 
   for (size_t c0 = 0; c0 < npairs_all; c0 += chunk) {
     const size_t npairs = std::min(chunk, npairs_all - c0);
-    const int nb = (strip.band_end < 0 ? bands : strip.band_end) - strip.band_begin;
+    const int nb = static_cast<int>(plan.owned_bands);
     const unsigned long long units = static_cast<unsigned long long>(npairs) * nb;
     int blocks = bps * c.sms;
     if (const char* e = std::getenv("SK_FORCE_BPS")) blocks = std::max(1, std::min(bps, std::atoi(e))) * c.sms;
@@ -519,6 +541,11 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
       const size_t fit = std::max<size_t>(1, budget / col_bytes);
       if (slots > fit) slots = std::max<size_t>(fit, 1);
       if (group > slots) group = slots;
+    }
+    // strips (one pair): one column buffer per block round
+    if (!whole) {
+      slots = plan.rounds;
+      group = 1;
     }
     // test hooks: force small groups / slot counts to exercise slot reuse
     if (const char* e = std::getenv("SK_FORCE_GROUP")) group = std::max<size_t>(1, std::min<size_t>(group, std::atoi(e)));
@@ -609,10 +636,11 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.diag = o.d_diag;
     P.grid_stride = o.grid_stride;
     P.diag_stride = o.diag_stride;
-    P.band_begin = strip.band_begin;
-    P.band_end = strip.band_end < 0 ? bands : strip.band_end;
-    P.xin_band = strip.xin_band;
-    P.xout_band = strip.xout_band;
+    P.xgpus = strip.gpus;
+    P.xrank = strip.rank;
+    P.xblock = static_cast<int>(sblock);
+    P.xexch = strip.exch ? 1 : 0;
+    P.units_pair_streaming = nb;
     P.xin_abuf = strip.xin_abuf;
     P.xin_prog = strip.xin_prog;
     P.xout_abuf = strip.xout_abuf;
@@ -1343,27 +1371,27 @@ int sk_strip_bands(size_t ly, int order, size_t* bands) {
   return SK_OK;
 }
 
-int sk_exchange_alloc(size_t lx, int order, void** abuf, void** prog, sk_status* st) {
+int sk_exchange_alloc(size_t lx, int order, size_t rounds, void** abuf, void** prog, sk_status* st) {
   clear_status(st);
-  if (lx < 2 || order < 1 || order > kMaxOrder)
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "exchange: bad length/order");
+  if (lx < 2 || order < 1 || order > kMaxOrder || rounds < 1)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "exchange: bad length/order/rounds");
   Ctx* cp = nullptr;
   if (int rc = get_ctx(&cp, st)) return rc;
-  const size_t bytes = (lx - 1) * np_of(order) * sizeof(double);
+  const size_t bytes = rounds * (lx - 1) * np_of(order) * sizeof(double);
   SK_CUDA(cudaMalloc(abuf, bytes));
-  SK_CUDA(cudaMalloc(prog, 256));
+  SK_CUDA(cudaMalloc(prog, rounds * kXProg * sizeof(unsigned long long)));
   // zeroed on the context's (non-blocking) stream and waited for: a legacy-
   // stream memset would not be ordered against the sweeps
-  SK_CUDA(cudaMemsetAsync(*prog, 0, 256, cp->stream()));
+  SK_CUDA(cudaMemsetAsync(*prog, 0, rounds * kXProg * sizeof(unsigned long long), cp->stream()));
   SK_CUDA(cudaStreamSynchronize(cp->stream()));
   return SK_OK;
 }
 
-int sk_exchange_reset(void* prog, sk_status* st) {
+int sk_exchange_reset(void* prog, size_t rounds, sk_status* st) {
   clear_status(st);
   Ctx* cp = nullptr;
   if (int rc = get_ctx(&cp, st)) return rc;
-  SK_CUDA(cudaMemsetAsync(prog, 0, 256, cp->stream()));
+  SK_CUDA(cudaMemsetAsync(prog, 0, rounds * kXProg * sizeof(unsigned long long), cp->stream()));
   SK_CUDA(cudaStreamSynchronize(cp->stream()));
   return SK_OK;
 }
@@ -1420,29 +1448,22 @@ int sk_enable_peer_access(int peer, sk_status* st) {
   return SK_OK;
 }
 
-// One strip of a long pair: bands [band_begin, band_end) of the 32R-row bands
-// (sk_strip_bands).  The bottom band (band_begin > 0) reads its alpha from
-// in_abuf / in_prog (device memory of this GPU, written by the previous
-// strip's GPU); the top band (band_end < bands) writes to out_abuf / out_prog
-// (the next GPU's exchange buffer, a peer pointer from sk_ipc_open).  All
-// strips of a pair run concurrently, one per GPU.  *value is written only by
-// the strip that owns the last row; diag (optional, min(lx,ly)-1 entries)
-// receives this strip's knots.
-int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
-                       size_t band_begin, size_t band_end, const void* in_abuf, const void* in_prog, void* out_abuf,
-                       void* out_prog, double* value, double* diag, sk_status* st) {
-  clear_status(st);
+int sk_strip_plan(size_t ly, int order, size_t gpus, size_t rank, size_t block, size_t* owned_bands,
+                  size_t* rounds, size_t* in_rounds) {
   size_t bands = 0;
-  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2)
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: bad arguments");
-  if (band_begin >= band_end || band_end > bands)
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: band range [%zu, %zu) outside [0, %zu)",
-                      band_begin, band_end, bands);
-  if ((band_begin > 0) != (in_abuf != nullptr) || (band_end < bands) != (out_abuf != nullptr))
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: exchange buffers do not match the range");
-  Ctx* cp = nullptr;
-  if (int rc = get_ctx(&cp, st)) return rc;
-  Ctx& c = *cp;
+  if (gpus < 1 || rank >= gpus || block < 1 || sk_strip_bands(ly, order, &bands) != SK_OK) return SK_INVALID_ARGUMENT;
+  const StripPlan pl = strip_plan(bands, gpus, rank, block);
+  if (owned_bands) *owned_bands = pl.owned_bands;
+  if (rounds) *rounds = pl.rounds;
+  if (in_rounds) *in_rounds = pl.in_rounds;
+  return SK_OK;
+}
+
+// Shared by sk_propagate_strip (one GPU of a multi-GPU pipeline) and
+// sk_propagate_split (every GPU of the pipeline emulated in ONE launch on one
+// GPU: gpus = 1, every block boundary still routed through an exchange area).
+static int strip_launch(Ctx& c, const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
+                        uint32_t flags, const Strip& s, double* value, double* diag, sk_status* st) {
   const size_t ld = inc_ld(dim);
   SK_CUDA(c.raw_x.ensure(lx * dim * sizeof(double)));
   SK_CUDA(c.raw_y.ensure(ly * dim * sizeof(double)));
@@ -1467,19 +1488,6 @@ int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, s
   PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), lx * ld, ly * ld, static_cast<int>(ly - 1),
              static_cast<int>(lx - 1), static_cast<int>(dim), static_cast<int>(ld)};
   Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(), nullptr, nullptr, d_diag, lx * ly, nd};
-  Strip s;
-  s.band_begin = static_cast<int>(band_begin);
-  s.band_end = static_cast<int>(band_end);
-  if (band_begin > 0) {
-    s.xin_band = static_cast<int>(band_begin);
-    s.xin_abuf = static_cast<const double*>(in_abuf);
-    s.xin_prog = static_cast<const unsigned long long*>(in_prog);
-  }
-  if (band_end < bands) {
-    s.xout_band = static_cast<int>(band_end) - 1;
-    s.xout_abuf = static_cast<double*>(out_abuf);
-    s.xout_prog = static_cast<unsigned long long*>(out_prog);
-  }
   std::vector<uint32_t> zero(1, 0);
   if (int rc = run_sweeps(c, ps, zero, zero, zero, order, flags | kFlagAllTotals, o, st, s)) return rc;
   unsigned long long key = ~0ull;
@@ -1488,62 +1496,82 @@ int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, s
   SK_CUDA(cudaMemcpyAsync(&v, c.values.p, sizeof v, cudaMemcpyDeviceToHost, c.stream()));
   if (diag) SK_CUDA(cudaMemcpyAsync(diag, d_diag, nd * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
   SK_CUDA(cudaStreamSynchronize(c.stream()));
-  if (key != ~0ull) {
+  if (key != ~0ull)
     return decode_err(key, st, device_delta(c, c.xinc.as<double>(), c.yinc.as<double>(), ld, dim, key));
-  }
-  if (band_end == bands && value) *value = v;
+  if (value) *value = v;
   return SK_OK;
 }
 
-// Single-GPU emulation of a two-strip pipeline: ONE launch sweeps every band
-// but routes the hand-off from band split-1 to band split through an
-// exchange buffer with system-scope release/acquire, exactly as two GPUs
-// would.  Used to test the strip path on one GPU (strips on one GPU may not
-// run as separate launches that wait on each other).
-int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
-                       size_t split_band, double* value, sk_status* st) {
+// One GPU's share of a long pair over `gpus` GPUs (block-cyclic: blocks of
+// `block` bands, GPU `rank` sweeps blocks rank, rank + gpus, ...).  in_abuf /
+// in_prog: this GPU's exchange area (sk_exchange_alloc with in_rounds of
+// sk_strip_plan), written by GPU rank - 1 (mod gpus); out_abuf / out_prog:
+// GPU rank + 1's area (peer pointers, sk_ipc_open or peer access).  All GPUs
+// of a pair run concurrently.  *value is written by the GPU that owns the last
+// band; diag (optional, min(lx,ly)-1 entries) receives this GPU's knots.
+int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
+                       size_t gpus, size_t rank, size_t block, const void* in_abuf, const void* in_prog,
+                       void* out_abuf, void* out_prog, double* value, double* diag, sk_status* st) {
   clear_status(st);
   size_t bands = 0;
-  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2 || split_band < 1 || split_band >= bands)
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_split: split band outside (0, bands)");
-  void *xa = nullptr, *xp = nullptr;
-  if (int rc = sk_exchange_alloc(lx, order, &xa, &xp, st)) return rc;
+  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: bad arguments");
+  if (gpus < 1 || rank >= gpus || block < 1)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: rank %zu of %zu GPUs, block %zu", rank, gpus,
+                      block);
+  const size_t nblocks = (bands + block - 1) / block;
+  const StripPlan pl = strip_plan(bands, gpus, rank, block);
+  // blocks other than the last hand up; whether this GPU sends / receives
+  bool sends = false;
+  for (size_t k = rank; k + 1 < nblocks; k += gpus) sends = true;
+  if ((pl.in_rounds > 0) != (in_abuf != nullptr && in_prog != nullptr) ||
+      (sends && gpus > 1) != (out_abuf != nullptr && out_prog != nullptr))
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_strip: exchange buffers do not match the plan");
   Ctx* cp = nullptr;
   if (int rc = get_ctx(&cp, st)) return rc;
-  Ctx& c = *cp;
-  const size_t ld = inc_ld(dim);
-  int rc = SK_OK;
-  do {
-    if (cudaError_t e = c.raw_x.ensure(lx * dim * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
-    if (cudaError_t e = c.raw_y.ensure(ly * dim * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
-    if (cudaError_t e = c.xinc.ensure(lx * ld * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
-    if (cudaError_t e = c.yinc.ensure(ly * ld * sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
-    if (cudaError_t e = c.values.ensure(sizeof(double)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
-    if (cudaError_t e = c.err.ensure(sizeof(unsigned long long)); e != cudaSuccess) { rc = cuda_fail(st, e, "alloc"); break; }
-    h2d(c, c.raw_x.p, x, lx * dim * sizeof(double));
-    h2d(c, c.raw_y.p, y, ly * dim * sizeof(double));
-    launch_increments(c.raw_x.as<double>(), 1, lx, dim, ld, c.xinc.as<double>(), c.stream());
-    launch_increments(c.raw_y.as<double>(), 1, ly, dim, ld, c.yinc.as<double>(), c.stream());
-    cudaMemsetAsync(c.err.p, 0xff, sizeof(unsigned long long), c.stream());
-    cudaMemsetAsync(c.values.p, 0xff, sizeof(double), c.stream());
-    PairSet ps{c.xinc.as<double>(), c.yinc.as<double>(), lx * ld, ly * ld, static_cast<int>(ly - 1),
-               static_cast<int>(lx - 1), static_cast<int>(dim), static_cast<int>(ld)};
-    Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(), nullptr, nullptr, nullptr, 0, 0};
+  Strip s;
+  s.gpus = static_cast<int>(gpus);
+  s.rank = static_cast<int>(rank);
+  s.block = static_cast<int>(block);
+  s.exch = gpus > 1;
+  s.xin_abuf = static_cast<const double*>(in_abuf);
+  s.xin_prog = static_cast<const unsigned long long*>(in_prog);
+  s.xout_abuf = static_cast<double*>(out_abuf);
+  s.xout_prog = static_cast<unsigned long long*>(out_prog);
+  double v = std::numeric_limits<double>::quiet_NaN();
+  if (int rc = strip_launch(*cp, x, lx, y, ly, dim, order, flags, s, &v, diag, st)) return rc;
+  if ((nblocks - 1) % gpus == rank && value) *value = v;
+  return SK_OK;
+}
+
+// One-GPU emulation of the strip pipeline: ONE launch sweeps every band, but
+// every `block` bands the hand-off goes through an exchange area with
+// system-scope release/acquire, exactly as between GPUs.  Used to test the
+// strip path on one GPU (strips on one GPU may not run as separate launches
+// that wait on each other).
+int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
+                       size_t block, double* value, sk_status* st) {
+  clear_status(st);
+  size_t bands = 0;
+  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2 || block < 1 || block >= bands)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_split: block outside [1, bands)");
+  const size_t nblocks = (bands + block - 1) / block;
+  void *xa = nullptr, *xp = nullptr;
+  if (int rc = sk_exchange_alloc(lx, order, nblocks, &xa, &xp, st)) return rc;
+  Ctx* cp = nullptr;
+  int rc = get_ctx(&cp, st);
+  if (rc == SK_OK) {
     Strip s;
-    s.xin_band = static_cast<int>(split_band);
-    s.xout_band = static_cast<int>(split_band) - 1;
+    s.gpus = 1;
+    s.rank = 0;
+    s.block = static_cast<int>(block);
+    s.exch = true;
     s.xin_abuf = static_cast<const double*>(xa);
     s.xout_abuf = static_cast<double*>(xa);
     s.xin_prog = static_cast<const unsigned long long*>(xp);
     s.xout_prog = static_cast<unsigned long long*>(xp);
-    std::vector<uint32_t> zero(1, 0);
-    if ((rc = run_sweeps(c, ps, zero, zero, zero, order, flags | kFlagAllTotals, o, st, s)) != SK_OK) break;
-    unsigned long long key = ~0ull;
-    cudaMemcpyAsync(&key, c.err.p, sizeof key, cudaMemcpyDeviceToHost, c.stream());
-    cudaMemcpyAsync(value, c.values.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream());
-    if (cudaError_t e = cudaStreamSynchronize(c.stream()); e != cudaSuccess) { rc = cuda_fail(st, e, "sync"); break; }
-    if (key != ~0ull) rc = decode_err(key, st, device_delta(c, c.xinc.as<double>(), c.yinc.as<double>(), ld, dim, key));
-  } while (false);
+    rc = strip_launch(*cp, x, lx, y, ly, dim, order, flags, s, value, nullptr, st);
+  }
   sk_exchange_free(xa, xp);
   return rc;
 }

@@ -104,15 +104,19 @@ struct SweepParams {
   double* grid;                   // per output slot: lx x ly knot grid, or null
   double* diag;                   // per output slot: K at tiles (i, i), or null
   unsigned long long grid_stride, diag_stride;
-  // Band range of this launch ([0, bands) normally; a strip of a long pair on
-  // one GPU of a multi-GPU pipeline otherwise) and the cross-strip hand-off:
-  // band xout_band writes its alpha' to xout_abuf / publishes xout_prog
-  // (peer memory of the next GPU, system-scope release), band xin_band reads
-  // xin_abuf / waits on xin_prog (written by the previous GPU).  -1: none.
-  int band_begin, band_end;
-  int xin_band, xout_band;
-  const double* xin_abuf;
-  const unsigned long long* xin_prog;
+  // Long pair over several GPUs (block-cyclic strips):
+  // the bands are cut into blocks of xblock bands dealt round-robin over
+  // xgpus GPUs -- this launch sweeps the blocks k with k mod xgpus == xrank,
+  // in increasing order (round r = k / xgpus), one column buffer per round.
+  // With xexch set, every block boundary hands alpha over through exchange
+  // buffers: block k's bottom band reads xin_abuf[r] / waits on xin_prog[r]
+  // (this GPU's memory, written by the GPU of block k - 1), block k's top band
+  // writes xout_abuf[r'] / publishes xout_prog[r'] (the next GPU's exchange
+  // area, peer memory; r' = (k + 1) / xgpus), system-scope release/acquire.
+  // One GPU, one launch: xgpus = 1, xblock = bands, xexch = 0.
+  int xgpus, xrank, xblock, xexch;
+  const double* xin_abuf;             // rounds x cols x NP
+  const unsigned long long* xin_prog;  // rounds x kXProg
   double* xout_abuf;
   unsigned long long* xout_prog;
   // Segment-DAG mode (seg_cols > 0): the unit is (pair, band, segment), a
@@ -125,6 +129,7 @@ struct SweepParams {
   // (rq); bands carry their lane state between segments in susp records.
   int seg_cols, segs_per_band;
   unsigned units_total;
+  int units_pair_streaming;  // bands per pair in this launch (streaming schedule)
   double* susp;
   unsigned* dep;
   unsigned* rq;   // ready list, units_total cells
@@ -132,6 +137,7 @@ struct SweepParams {
 };
 
 constexpr int kCtrLine = 32;  // u32 words per counter line
+constexpr int kXProg = 16;    // u64 words between exchange progress counters (128 B)
 
 // sweep_band outcomes
 constexpr int kBandDone = 0, kBandAbort = 2;
@@ -427,7 +433,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const int rows = P.rows, cols = P.cols;
   const int row0 = static_cast<int>(b) * 32 * R;
   const int rb = min(32 * R, rows - row0);
-  const unsigned slot = p % static_cast<unsigned>(P.slots);
+  // strips: one column buffer per block round; pairs: slot of the pair
+  const unsigned blk = b / static_cast<unsigned>(P.xblock);
+  const unsigned slot = P.xgpus > 1 || P.xexch ? blk / static_cast<unsigned>(P.xgpus)
+                                               : p % static_cast<unsigned>(P.slots);
   const unsigned long long base = static_cast<unsigned long long>(p) * static_cast<unsigned long long>(cols + 1);
   double* colbuf = P.abuf + static_cast<size_t>(slot) * static_cast<size_t>(cols) * NP;
   unsigned long long* prog_row = P.prog + static_cast<size_t>(slot) * P.bands;
@@ -435,12 +444,15 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const bool has_above = b + 1 < static_cast<unsigned>(P.bands);
   // where this band's alpha comes from / goes to: the pair's column buffer,
   // or a cross-strip exchange buffer (multi-GPU long pair)
-  const bool xin = static_cast<int>(b) == P.xin_band;
-  const bool xout = static_cast<int>(b) == P.xout_band;
-  const double* in_buf = xin ? P.xin_abuf : colbuf;
-  const unsigned long long* in_prog = xin ? P.xin_prog : prog_row + (has_below ? b - 1 : 0);
-  double* out_buf = xout ? P.xout_abuf : colbuf;
-  unsigned long long* out_prog = xout ? P.xout_prog : prog_row + b;
+  const bool xin = P.xexch && has_below && b % static_cast<unsigned>(P.xblock) == 0;
+  const bool xout = P.xexch && has_above && (b + 1) % static_cast<unsigned>(P.xblock) == 0;
+  const size_t xstride = static_cast<size_t>(cols) * NP;
+  const unsigned rin = blk / static_cast<unsigned>(P.xgpus);
+  const unsigned rout = (blk + 1) / static_cast<unsigned>(P.xgpus);
+  const double* in_buf = xin ? P.xin_abuf + rin * xstride : colbuf;
+  const unsigned long long* in_prog = xin ? P.xin_prog + rin * kXProg : prog_row + (has_below ? b - 1 : 0);
+  double* out_buf = xout ? P.xout_abuf + rout * xstride : colbuf;
+  unsigned long long* out_prog = xout ? P.xout_prog + rout * kXProg : prog_row + b;
   const unsigned out = P.pair_out[p];
   const bool strict = (P.flags & kFlagStrictCorner) != 0;
   const bool fault = (P.flags & kFlagWFault) != 0;
@@ -1086,7 +1098,8 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 ? 1 : sweep_m
   }
   constexpr int H = 32 * rows_per_lane(N);
   constexpr int K = chunk_cols(rows_per_lane(N));
-  const unsigned nb = static_cast<unsigned>(P.band_end - P.band_begin);
+  // bands of each pair this launch sweeps (all, or this GPU's strip blocks)
+  const unsigned nb = static_cast<unsigned>(P.units_pair_streaming);
   const unsigned gsz = static_cast<unsigned>(P.group) * nb;
   // one unit; DP == 0: hand it to the producer warp first, and meet it again
   // at the end (the ring is reused by the next unit)
@@ -1128,8 +1141,11 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 ? 1 : sweep_m
       const unsigned rem = u - g * gsz;
       const unsigned g0 = g * static_cast<unsigned>(P.group);
       const unsigned gcount = min(static_cast<unsigned>(P.group), static_cast<unsigned>(P.npairs) - g0);
-      b = static_cast<unsigned>(P.band_begin) + rem / gcount;
-      p = g0 + (rem - (b - static_cast<unsigned>(P.band_begin)) * gcount);
+      const unsigned bi = rem / gcount;  // the pair's bi-th band of this launch
+      p = g0 + (rem - bi * gcount);
+      // strips: bi-th band of the blocks xrank, xrank + xgpus, ...
+      const unsigned S = static_cast<unsigned>(P.xblock);
+      b = (static_cast<unsigned>(P.xrank) + static_cast<unsigned>(P.xgpus) * (bi / S)) * S + bi % S;
     } else {
       // segment DAG: claim the next cell of the ready list, wait for its unit
       unsigned u = 0;

@@ -120,9 +120,37 @@ def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] 
 
 
 # ------------------------------------------------------------ long pairs
+# Resident band workers of one B200 at the register kernels' 12 one-warp CTAs
+# per SM: the block size of the cyclic strip layout.
+BAND_WORKERS = 12 * 148
+
+
 def strip_ranges(bands: int, world: int):
-    """Contiguous, balanced band ranges [b0, b1) of a long pair, one per rank."""
+    """Contiguous, balanced band ranges [b0, b1), one per rank (round 1's
+    layout; kept for the error-order helpers and comparisons)."""
     return [(bands * g // world, bands * (g + 1) // world) for g in range(world)]
+
+
+def strip_block(bands: int, world: int, workers: int = BAND_WORKERS) -> int:
+    """Block size of the block-cyclic layout: the bands split into
+    world x rounds equal blocks, rounds = ceil(bands / (world x workers)),
+    so a GPU's block never exceeds its resident band workers."""
+    rounds = max(1, -(-bands // (world * workers)))
+    return max(1, -(-bands // (world * rounds)))
+
+
+def strip_plan(ly: int, order: int, world: int, rank: int, block: int):
+    """(owned bands, column-buffer rounds, exchange rounds received) of rank
+    `rank` in the block-cyclic layout (sk_strip_plan)."""
+    o, r, i = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    if _capi.load().sk_strip_plan(ly, int(order), world, rank, block, ctypes.byref(o), ctypes.byref(r),
+                                  ctypes.byref(i)) != 0:
+        raise ValueError("strip_plan: bad arguments")
+    return o.value, r.value, i.value
+
+
+def block_owner(band: int, world: int, block: int) -> int:
+    return (band // block) % world
 
 
 def first_error(records):
@@ -140,14 +168,27 @@ def first_error(records):
     return None if best is None else best[1]
 
 
+def _raise_first(recs):
+    err = first_error(recs)
+    if err is not None:
+        code, k, l, msg = err
+        if code == _capi.SK_NUMERIC_OVERFLOW:
+            raise sk.NumericOverflowError(msg, k, l)
+        if code == _capi.SK_INCONSISTENT_BOUNDARY:
+            raise sk.InconsistentBoundaryError(msg)
+        raise RuntimeError(msg)
+
+
 def propagate_long_pair_distributed(x, y, order: int, options: Optional[sk.PropagateOptions] = None,
-                                    group=None, diag: bool = False):
-    """K(1,1) of ONE long pair split into row strips across the ranks of
-    `group` (one process per GPU): rank g sweeps a
-    contiguous band range and streams its top band's alpha series straight
-    into rank g+1's exchange buffer over NVLink (CUDA IPC peer mapping,
-    system-scope release/acquire).  Every rank returns (value, diag-or-None);
-    diag holds this rank's knots K(a, a) (NaN elsewhere)."""
+                                    group=None, diag: bool = False, block: Optional[int] = None):
+    """K(1,1) of ONE long pair over the ranks of `group` (one process per GPU,
+    SURVEY.md section 8e), block-cyclic: the 32-row bands are cut into blocks
+    of `block` bands (default strip_block) dealt round-robin over the ranks;
+    at every block boundary the top band streams its alpha series straight
+    into the next rank's exchange area over NVLink (CUDA IPC peer mapping,
+    system-scope release/acquire; the last rank hands to rank 0).  Every rank
+    returns (value, diag-or-None); diag holds this rank's knots K(a, a)
+    (NaN elsewhere)."""
     import torch.distributed as dist
 
     x, y = sk._as_series(x), sk._as_series(y)
@@ -157,72 +198,67 @@ def propagate_long_pair_distributed(x, y, order: int, options: Optional[sk.Propa
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     lx, ly, d = x.length(), y.length(), x.dim()
-    nb = ctypes.c_size_t()
-    if lib.sk_strip_bands(ly, int(order), ctypes.byref(nb)) != 0:
-        raise ValueError("propagate: bad length/order")
-    bands = nb.value
-    if bands < world:
-        raise ValueError(f"{bands} bands cannot feed {world} GPUs")
-    b0, b1 = strip_ranges(bands, world)[rank]
+    bands = strip_bands(ly, order)
+    block = block or strip_block(bands, world)
+    nblocks = -(-bands // block)
+    if nblocks < world:
+        raise ValueError(f"{nblocks} blocks of {block} bands cannot feed {world} GPUs")
+    _, _, in_rounds = strip_plan(ly, order, world, rank, block)
+    sends = any(k + 1 < nblocks for k in range(rank, nblocks, world))
     st = _capi.SkStatus()
     in_a, in_p, out_a, out_p = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     handles = None
-    if rank > 0:
-        sk._check(lib.sk_exchange_alloc(lx, int(order), ctypes.byref(in_a), ctypes.byref(in_p), ctypes.byref(st)), st)
+    if world > 1 and in_rounds > 0:
+        sk._check(lib.sk_exchange_alloc(lx, int(order), in_rounds, ctypes.byref(in_a), ctypes.byref(in_p),
+                                        ctypes.byref(st)), st)
         ha, hp = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
         sk._check(lib.sk_ipc_handle(in_a, ha, ctypes.byref(st)), st)
         sk._check(lib.sk_ipc_handle(in_p, hp, ctypes.byref(st)), st)
         handles = (bytes(ha), bytes(hp))
     all_handles = [None] * world
     dist.all_gather_object(all_handles, handles, group=group)
+    nxt = (rank + 1) % world
     try:
-        if rank + 1 < world:
-            ha, hp = all_handles[rank + 1]
+        if world > 1 and sends:
+            ha, hp = all_handles[nxt]
             sk._check(lib.sk_ipc_open(ctypes.create_string_buffer(ha, 64), ctypes.byref(out_a), ctypes.byref(st)), st)
             sk._check(lib.sk_ipc_open(ctypes.create_string_buffer(hp, 64), ctypes.byref(out_p), ctypes.byref(st)), st)
         dist.barrier(group=group)
         value = ctypes.c_double(float("nan"))
         dg = np.full(min(lx, ly) - 1, np.nan) if diag else None
         xv, yv = x.values(), y.values()
-        rc = lib.sk_propagate_strip(sk._ptr(xv), lx, sk._ptr(yv), ly, d, int(order), sk._flags(options), b0, b1,
-                                    in_a if rank > 0 else None, in_p if rank > 0 else None,
-                                    out_a if rank + 1 < world else None, out_p if rank + 1 < world else None,
+        rc = lib.sk_propagate_strip(sk._ptr(xv), lx, sk._ptr(yv), ly, d, int(order), sk._flags(options), world, rank,
+                                    block, in_a if in_a.value else None, in_p if in_p.value else None,
+                                    out_a if out_a.value else None, out_p if out_p.value else None,
                                     ctypes.byref(value), sk._ptr(dg) if dg is not None else None, ctypes.byref(st))
         rec = None if rc == 0 else (int(st.code), int(st.tile_k), int(st.tile_l), st.message.decode(errors="replace"))
         recs = [None] * world
-        dist.all_gather_object(recs, (rec, value.value if b1 == bands else None), group=group)
+        owner_last = (nblocks - 1) % world
+        dist.all_gather_object(recs, (rec, value.value if rank == owner_last else None), group=group)
     finally:
         dist.barrier(group=group)
-        if rank + 1 < world:
-            if out_a.value:
-                lib.sk_ipc_close(out_a)
-            if out_p.value:
-                lib.sk_ipc_close(out_p)
-        if rank > 0:
+        if out_a.value:
+            lib.sk_ipc_close(out_a)
+        if out_p.value:
+            lib.sk_ipc_close(out_p)
+        if in_a.value:
             lib.sk_exchange_free(in_a, in_p)
-    err = first_error([r for r, _ in recs])
-    if err is not None:
-        code, k, l, msg = err
-        if code == _capi.SK_NUMERIC_OVERFLOW:
-            raise sk.NumericOverflowError(msg, k, l)
-        if code == _capi.SK_INCONSISTENT_BOUNDARY:
-            raise sk.InconsistentBoundaryError(msg)
-        raise RuntimeError(msg)
+    _raise_first([r for r, _ in recs])
     final = [v for _, v in recs if v is not None][0]
     return final, dg
 
 
-def propagate_split_emulated(x, y, order: int, split_band: int, options: Optional[sk.PropagateOptions] = None):
-    """One-GPU test of the strip protocol: a single launch whose hand-off from
-    band split_band-1 to split_band goes through an exchange buffer exactly
-    as between two GPUs (sk_propagate_split)."""
+def propagate_split_emulated(x, y, order: int, block: int, options: Optional[sk.PropagateOptions] = None):
+    """One-GPU test of the strip protocol: a single launch whose hand-off
+    every `block` bands goes through an exchange area exactly as between
+    GPUs (sk_propagate_split)."""
     x, y = sk._as_series(x), sk._as_series(y)
     lib = _capi.load()
     st = _capi.SkStatus()
     value = ctypes.c_double()
     xv, yv = x.values(), y.values()
     rc = lib.sk_propagate_split(sk._ptr(xv), x.length(), sk._ptr(yv), y.length(), x.dim(), int(order),
-                                sk._flags(options), int(split_band), ctypes.byref(value), ctypes.byref(st))
+                                sk._flags(options), int(block), ctypes.byref(value), ctypes.byref(st))
     sk._check(rc, st)
     return value.value
 
@@ -235,18 +271,17 @@ def strip_bands(ly: int, order: int) -> int:
 
 
 def propagate_long_pair_devices(x, y, order: int, devices: Sequence[int],
-                                options: Optional[sk.PropagateOptions] = None, diag: bool = False):
-    """K(1,1) of ONE long pair split into row strips over several GPUs driven
-    from this process (the SURVEY.md section 8b device-list option; the
-    multi-process variant is propagate_long_pair_distributed).  Strip g runs
-    on devices[g] in its own host thread; its top band writes alpha' straight
-    into devices[g+1]'s exchange buffer through peer access (NVLink), with the
-    same system-scope release/acquire protocol.  Returns (value, diag-or-None).
-    The devices must be distinct: strips wait on each other, so two of them
-    must never share a GPU (one GPU: sk.propagate)."""
+                                options: Optional[sk.PropagateOptions] = None, diag: bool = False,
+                                block: Optional[int] = None):
+    """K(1,1) of ONE long pair over several GPUs driven from this process (the
+    SURVEY.md section 8b device-list option; the multi-process variant is
+    propagate_long_pair_distributed): the same block-cyclic layout, one host
+    thread per device, exchange areas reached through peer access (NVLink).
+    Returns (value, diag-or-None).  The devices must be distinct: GPUs wait on
+    each other, so two of them must never share one (one GPU: sk.propagate)."""
     import threading
 
-    devices = [int(d) for d in devices]
+    devices = [int(dv) for dv in devices]
     if len(set(devices)) != len(devices):
         raise ValueError("propagate_long_pair_devices: devices must be distinct (strips wait on each other)")
     x, y = sk._as_series(x), sk._as_series(y)
@@ -263,20 +298,25 @@ def propagate_long_pair_devices(x, y, order: int, devices: Sequence[int],
     lx, ly, d = x.length(), y.length(), x.dim()
     world = len(devices)
     bands = strip_bands(ly, order)
-    if bands < world:
-        raise ValueError(f"{bands} bands cannot feed {world} GPUs")
-    ranges = strip_ranges(bands, world)
+    block = block or strip_block(bands, world)
+    nblocks = -(-bands // block)
+    if nblocks < world:
+        raise ValueError(f"{nblocks} blocks of {block} bands cannot feed {world} GPUs")
     st = _capi.SkStatus()
-    xbuf = [None] * world  # exchange buffer (abuf, prog) on each consumer device
+    xbuf = [None] * world  # exchange area (abuf, prog) on each receiving device
     try:
-        for g in range(1, world):
+        for g in range(world):
+            _, _, in_rounds = strip_plan(ly, order, world, g, block)
+            if in_rounds == 0:
+                continue
             sk._check(lib.sk_set_device(devices[g], ctypes.byref(st)), st)
             a, p = ctypes.c_void_p(), ctypes.c_void_p()
-            sk._check(lib.sk_exchange_alloc(lx, int(order), ctypes.byref(a), ctypes.byref(p), ctypes.byref(st)), st)
+            sk._check(lib.sk_exchange_alloc(lx, int(order), in_rounds, ctypes.byref(a), ctypes.byref(p),
+                                            ctypes.byref(st)), st)
             xbuf[g] = (a, p)
-        for g in range(world - 1):
+        for g in range(world):
             sk._check(lib.sk_set_device(devices[g], ctypes.byref(st)), st)
-            sk._check(lib.sk_enable_peer_access(devices[g + 1], ctypes.byref(st)), st)
+            sk._check(lib.sk_enable_peer_access(devices[(g + 1) % world], ctypes.byref(st)), st)
         xv, yv = x.values(), y.values()
         out = [None] * world
         dg = np.full(min(lx, ly) - 1, np.nan) if diag else None
@@ -287,11 +327,11 @@ def propagate_long_pair_devices(x, y, order: int, devices: Sequence[int],
             v = ctypes.c_double(float("nan"))
             rc = lib.sk_set_device(devices[g], ctypes.byref(s))
             if rc == 0:
-                b0, b1 = ranges[g]
-                rc = lib.sk_propagate_strip(sk._ptr(xv), lx, sk._ptr(yv), ly, d, int(order), sk._flags(options), b0, b1,
-                                            xbuf[g][0] if g > 0 else None, xbuf[g][1] if g > 0 else None,
-                                            xbuf[g + 1][0] if g + 1 < world else None,
-                                            xbuf[g + 1][1] if g + 1 < world else None, ctypes.byref(v),
+                sends = any(k + 1 < nblocks for k in range(g, nblocks, world))
+                inn, nxt = xbuf[g], xbuf[(g + 1) % world] if sends else None
+                rc = lib.sk_propagate_strip(sk._ptr(xv), lx, sk._ptr(yv), ly, d, int(order), sk._flags(options),
+                                            world, g, block, inn[0] if inn else None, inn[1] if inn else None,
+                                            nxt[0] if nxt else None, nxt[1] if nxt else None, ctypes.byref(v),
                                             sk._ptr(parts[g]) if diag else None, ctypes.byref(s))
             out[g] = (rc, s, v.value)
 
@@ -301,21 +341,13 @@ def propagate_long_pair_devices(x, y, order: int, devices: Sequence[int],
         for t in threads:
             t.join()
     finally:
-        for g in range(1, world):
+        for g in range(world):
             if xbuf[g] is not None:
                 lib.sk_exchange_free(xbuf[g][0], xbuf[g][1])
-    recs = [None if rc == 0 else (int(s.code), int(s.tile_k), int(s.tile_l), s.message.decode(errors="replace"))
-            for rc, s, _ in out]
-    err = first_error(recs)
-    if err is not None:
-        code, k, l, msg = err
-        if code == _capi.SK_NUMERIC_OVERFLOW:
-            raise sk.NumericOverflowError(msg, k, l)
-        if code == _capi.SK_INCONSISTENT_BOUNDARY:
-            raise sk.InconsistentBoundaryError(msg)
-        raise RuntimeError(msg)
+    _raise_first([None if rc == 0 else (int(s.code), int(s.tile_k), int(s.tile_l), s.message.decode(errors="replace"))
+                  for rc, s, _ in out])
     if diag:
         for g in range(world):
             sel = ~np.isnan(parts[g])
             dg[sel] = parts[g][sel]
-    return out[-1][2], dg
+    return out[(nblocks - 1) % world][2], dg

@@ -469,18 +469,19 @@ def test_gram_shards_reassemble(sk, restatement):
 
 # ------------------------------------------------------- multi-GPU strips
 def test_strip_protocol_emulated_on_one_gpu(sk, restatement):
-    """The long-pair strip hand-off (system-scope release/acquire through an
-    exchange buffer) inside one launch: bit-identical to the plain sweep."""
+    """The long-pair strip hand-off (system-scope release/acquire through the
+    exchange areas, every `block` bands -- block = 1: at every band boundary)
+    inside one launch: bit-identical to the plain sweep, knots included."""
     from paper_2502_20392_b200.distributed import propagate_split_emulated, strip_bands
-    for d in (4, 12, 40):  # register kernel with shared-memory / direct top-row hand-up, table path
+    for d in (4, 12, 40):  # register kernel with shared-memory / direct top-row hand-up, large-d path
         x = restatement.brownian(300, d, 5)
         y = restatement.brownian(400, d, 6)
         for order in (8, 20):
             plain = sk.propagate(x, y, order).value
             nb = strip_bands(400, order)
             assert nb >= 3
-            for split in range(1, nb):
-                assert propagate_split_emulated(x, y, order, split) == plain, (d, order, split)
+            for block in range(1, nb):
+                assert propagate_split_emulated(x, y, order, block) == plain, (d, order, block)
 
 
 def test_gram_over_a_device_list_matches_one_call(sk, restatement):

@@ -245,6 +245,42 @@ def test_strip_partition_and_error_order():
     assert first_error([None, None]) is None
 
 
+def test_block_cyclic_strip_plan():
+    """The block-cyclic long-pair layout (sk_strip_plan / distributed.py):
+    every band is owned by exactly one GPU, blocks are dealt round-robin, a
+    GPU's exchange rounds are the blocks >= 1 it owns, block sizes never
+    exceed the resident band workers, and the host model (tools/strip_sim.py)
+    scales where the contiguous layout of round 1 does not."""
+    from paper_2502_20392_b200.distributed import BAND_WORKERS, block_owner, strip_bands, strip_block, strip_plan
+    for ly, world in ((400, 1), (400, 3), (1_000_001, 8), (65_537, 2), (33, 1)):
+        bands = strip_bands(ly, 8)
+        for block in (1, 2, 5, strip_block(bands, world)):
+            if -(-bands // block) < world:
+                continue
+            owned = [0] * world
+            for b in range(bands):
+                owned[block_owner(b, world, block)] += 1
+            nblocks = -(-bands // block)
+            for g in range(world):
+                o, rounds, in_rounds = strip_plan(ly, 8, world, g, block)
+                mine = list(range(g, nblocks, world))
+                assert o == owned[g]
+                assert rounds == len(mine)
+                assert in_rounds == (max(mine) // world + 1 if any(k >= 1 for k in mine) else 0)
+    bands = strip_bands(1_000_001, 8)
+    for world in (1, 2, 4, 8):
+        assert strip_block(bands, world) <= BAND_WORKERS
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import strip_sim
+    # more bands per GPU than resident workers: contiguous strips starve
+    kw = dict(dt_ns=100_000.0, workers=100)
+    t1 = strip_sim.simulate(49_999, 2_000, 1, **kw)
+    t4c = strip_sim.simulate(49_999, 2_000, 4, "cyclic", block=100, **kw)
+    t4s = strip_sim.simulate(49_999, 2_000, 4, "contiguous", **kw)
+    assert t4c < 0.5 * t4s
+    assert t1 / (4 * t4c) > 0.8
+
+
 def test_segment_dag_model():
     """The segment-DAG schedule's dependency rules (tools/segment_dag_sim.py
     mirrors csrc/sk_sweep.cuh): every unit runs once, after its inputs, for
