@@ -176,7 +176,7 @@ struct Ctx {
   cudaStream_t user = nullptr;
   int sms = 148;
   DevBuf raw_x, raw_y, xinc, yinc, sqn, pairs, values, err, maxr, prog, queue, abuf, tab, grid, diag, w65, tile_io,
-      scan, wd, susp, dep, rq, redo, redo_out, gpairs;
+      scan, wd, susp, dep, rq, redo, redo_out, gpairs, maxall;
   bool stats_on = false;
   std::vector<StatRec> stats;
   std::vector<sk_gram_failure> failures;  // the last sk_gram / sk_gram_device call's entry failures
@@ -202,7 +202,7 @@ struct Ctx {
     }
     DevBuf* all[] = {&raw_x, &raw_y, &xinc, &yinc, &sqn, &pairs, &values, &err, &maxr,
                      &prog,  &queue, &abuf, &tab, &grid, &diag, &w65,   &tile_io, &scan, &wd,
-                     &susp,  &dep,   &rq,   &redo, &redo_out, &gpairs};
+                     &susp,  &dep,   &rq,   &redo, &redo_out, &gpairs, &maxall};
     for (DevBuf* b : all) b->release();
     if (own) cudaStreamDestroy(own);
   }
@@ -266,6 +266,7 @@ struct Outputs {
   double* d_grid;                // may be null
   double* d_diag;                // may be null
   unsigned long long grid_stride, diag_stride;
+  unsigned long long* d_maxrho_all = nullptr;  // only the launch-wide max|rho| is wanted (SweepParams)
 };
 
 double flops_per_tile(int order, int dim) {
@@ -412,7 +413,12 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
                const Strip& strip = Strip{}) {
   const size_t npairs_all = px.size();
   if (npairs_all == 0) return SK_OK;
-  const int ntempl = order <= kMaxRegOrder && !(flags & kFlagLiteral) ? order : 0;
+  // test hook: every sweep with the reference's literal arithmetic
+  if (const char* e = std::getenv("SK_FORCE_LITERAL"); e && e[0] == '1') flags |= kFlagLiteral | kFlagAllTotals;
+  // literal re-sweeps run the register-resident literal kernel where it is
+  // instantiated (order 8), the runtime-order literal kernel otherwise
+  const bool lit = (flags & kFlagLiteral) && order == 8 && std::getenv("SK_NO_LIT_REG") == nullptr;
+  const int ntempl = order <= kMaxRegOrder && (!(flags & kFlagLiteral) || lit) ? order : 0;
   const int dp = pick_dp(ps.dim);
   const int na = ntempl > 0 ? ntempl + 1 : kMaxOrder + 1;
   const int np = (na + 1) & ~1;
@@ -420,13 +426,13 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   const int band_rows = 32 * rows_per_lane(ntempl);  // 64-row bands for the register kernels
   const int bands = (rows + band_rows - 1) / band_rows;
   int bps = 0;
-  const bool exact = o.d_maxrho != nullptr;
-  const bool extras = o.d_grid != nullptr || o.d_diag != nullptr;
-  const int okey = ((ntempl * 32 + dp) * 2 + (exact ? 1 : 0)) * 2 + (extras ? 1 : 0);
+  const bool exact = o.d_maxrho != nullptr || lit;
+  const bool extras = o.d_grid != nullptr || o.d_diag != nullptr || lit;
+  const int okey = (((ntempl * 32 + dp) * 2 + (exact ? 1 : 0)) * 2 + (extras ? 1 : 0)) * 2 + (lit ? 1 : 0);
   if (auto it = c.occupancy.find(okey); it != c.occupancy.end()) {
     bps = it->second;
   } else {
-    SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, &bps));
+    SK_CUDA(sweep_occupancy(ntempl, dp, exact, extras, lit, &bps));
     c.occupancy[okey] = bps;
   }
   if (bps < 1) return set_status(st, SK_CUDA_ERROR, 0, 0, "sweep kernel cannot be resident (occupancy 0)");
@@ -444,7 +450,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // sequential one only where it could raise the exact max: they need a bound
   // on |fused - sequential| <= 2 d u sum|x_c y_c| <= 2 d u max||dx|| max||dy||
   double dot_err = 0.0;
-  if (exact && ntempl > 0) {
+  if (exact && ntempl > 0 && !lit) {
     const uint32_t nx = 1 + *std::max_element(px.begin(), px.end());
     const uint32_t ny = 1 + *std::max_element(py.begin(), py.end());
     SK_CUDA(c.sqn.ensure((nx + ny) * sizeof(double)));
@@ -594,7 +600,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
       // exact (sequential) deltas for the literal kernel, DMMA otherwise (the
       // EXACT max|rho| re-forms candidates with the sequential dot)
       SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, ps.dim, ps.ld,
-                               ntempl == 0, c.tab.as<double>(), tab_elems, c.stream()));
+                               ntempl == 0 || lit, c.tab.as<double>(), tab_elems, c.stream()));
       ++c.aux_launches;
     }
     SweepParams P{};
@@ -632,6 +638,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.values = o.d_values;
     P.err = o.d_err;
     P.maxrho = o.d_maxrho;
+    P.maxrho_all = o.d_maxrho_all;
     P.grid = o.d_grid;
     P.diag = o.d_diag;
     P.grid_stride = o.grid_stride;
@@ -657,7 +664,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     rec.tiles = static_cast<double>(npairs) * rows * cols;
     rec.flops = rec.tiles * flops_per_tile(order, ps.dim);
     if (int rc = record_start(c, &rec, st)) return rc;
-    SK_CUDA(sweep_launch(ntempl, dp, exact, extras, blocks, c.stream(), P));
+    SK_CUDA(sweep_launch(ntempl, dp, exact, extras, lit, blocks, c.stream(), P));
     if (int rc = record_end(c, &rec, st)) return rc;
     ++c.sweep_launches;
     if (int rc = check_watchdog(c, st)) return rc;
@@ -933,7 +940,8 @@ struct GramCore {
 };
 
 int gram_core(Ctx& c, const double* d_family, size_t m, size_t len, size_t dim, int adaptive, int order, double tol,
-              uint32_t flags, bool want_max, size_t t0, size_t t1, GramCore& g, sk_status* st) {
+              uint32_t flags, bool want_max, bool per_pair_max, size_t t0, size_t t1, GramCore& g,
+              sk_status* st) {
   c.failures.clear();
   const size_t np = t1 - t0;
   if (np == 0) return SK_OK;
@@ -987,6 +995,12 @@ int gram_core(Ctx& c, const double* d_family, size_t m, size_t len, size_t dim, 
   }
   Outputs o{c.values.as<double>(), c.err.as<unsigned long long>(),
             want_max ? c.maxr.as<unsigned long long>() : nullptr, nullptr, nullptr, 0, 0};
+  if (want_max && !per_pair_max) {
+    // only the family's maximum is reported: one running max for the launch
+    SK_CUDA(c.maxall.ensure(sizeof(unsigned long long)));
+    SK_CUDA(cudaMemsetAsync(c.maxall.p, 0, sizeof(unsigned long long), c.stream()));
+    o.d_maxrho_all = c.maxall.as<unsigned long long>();
+  }
   std::vector<int> distinct(g.ords.begin(), g.ords.end());
   std::sort(distinct.begin(), distinct.end());
   distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
@@ -1287,7 +1301,8 @@ int sk_gram(const double* family, size_t m, size_t len, size_t dim, int adaptive
   SK_CUDA(h2d(c, c.raw_x.p, family, m * len * dim * sizeof(double)));
   GramCore g;
   const bool want_max = scan_products != 0;
-  if (int rc = gram_core(c, c.raw_x.as<double>(), m, len, dim, adaptive, order, tol, flags, want_max, t0, t1, g, st))
+  if (int rc = gram_core(c, c.raw_x.as<double>(), m, len, dim, adaptive, order, tol, flags, want_max,
+                         pair_max != nullptr, t0, t1, g, st))
     return rc;
   double best = 0.0;
   for (size_t t = 0; t < g.pi.size(); ++t) {
@@ -1326,7 +1341,7 @@ int sk_gram_device(const double* d_family, size_t m, size_t len, size_t dim, int
   if (first == last) return SK_OK;
   GramCore g;
   const bool want_max = scan_products != 0;
-  if (int rc = gram_core(c, d_family, m, len, dim, adaptive, order, tol, flags, want_max, first, last, g, st))
+  if (int rc = gram_core(c, d_family, m, len, dim, adaptive, order, tol, flags, want_max, false, first, last, g, st))
     return rc;
   // values (NaN for failed entries) into the mirrored matrix cells
   const size_t np = g.pi.size();

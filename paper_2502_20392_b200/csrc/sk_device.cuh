@@ -254,6 +254,52 @@ __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// The same literal tile step with a compile-time order: series and partial
+// sums in registers, W from compile-time constants (tile_series.cpp:41-53:
+// factorials by repeated multiplication, then |a-b|! / (a! b!), evaluated in
+// IEEE double at compile time -- the same doubles; checked bitwise against the
+// device W table by the literal parity tests).  Strict-corner re-sweeps of
+// register-kernel pairs use it: ~40x shorter per tile than the runtime-order
+// kernel's local-memory arrays.  `fault` negates W[1][1] (the negative control).
+__host__ __device__ constexpr double cfact(int k) {
+  double f = 1.0;
+  for (int m = 1; m <= k; ++m) f *= static_cast<double>(m);
+  return f;
+}
+__host__ __device__ constexpr double cweight(int a, int b) {
+  return cfact(a > b ? a - b : b - a) / (cfact(a > b ? a : b) * cfact(a > b ? b : a));
+}
+
+template <int N>
+__device__ __forceinline__ double tile_step_literal_reg(const double (&alpha)[N + 1], const double (&beta)[N + 1],
+                                                        double delta, double (&out_alpha)[N + 1],
+                                                        double (&out_beta)[N + 1], bool fault) {
+  constexpr int n = N + 1;
+  double pw[n];
+  pw[0] = 1.0;
+#pragma unroll
+  for (int m = 1; m < n; ++m) pw[m] = __dmul_rn(pw[m - 1], delta);
+#pragma unroll
+  for (int j = 0; j < n; ++j) out_beta[j] = 0.0;
+  double total = 0.0;
+#pragma unroll
+  for (int i = 0; i < n; ++i) {
+    double row_sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const double b = (i >= j) ? alpha[i - j] : beta[j - i];
+      double w = cweight(i, j);
+      if (i == 1 && j == 1) w = fault ? -w : w;
+      const double val = __dmul_rn(b, __dmul_rn(pw[i < j ? i : j], w));
+      row_sum = __dadd_rn(row_sum, val);
+      out_beta[j] = __dadd_rn(out_beta[j], val);
+    }
+    out_alpha[i] = row_sum;
+    total = __dadd_rn(total, row_sum);
+  }
+  return total;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

@@ -59,8 +59,10 @@ cudaError_t launch_step_tile_fast(double delta, int order, const double* in, dou
 // exact: reference-identical delta (sequential non-FMA dot) + per-pair
 // max|delta| tracking; otherwise an FMA dot and no max tracking.
 // extras: knot grid / diagonal outputs.
-cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, int grid, cudaStream_t stream,
+// literal: the reference's arithmetic at this compile-time order (registers;
+// n_template 8 only) -- strict-corner re-sweeps.
+cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, bool literal, int grid, cudaStream_t stream,
                          const SweepParams& P);
-cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, int* blocks_per_sm);
+cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, bool literal, int* blocks_per_sm);
 
 }  // namespace skb

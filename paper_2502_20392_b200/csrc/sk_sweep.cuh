@@ -101,6 +101,11 @@ struct SweepParams {
   double* values;                 // per output slot: K(1,1)
   unsigned long long* err;        // per output slot: min error key (init ~0)
   unsigned long long* maxrho;     // per output slot: max |delta| bits (init 0) or null
+  // Only the maximum over every pair of the launch is wanted (a Gram's
+  // max_abs_increment_product without per-pair values): one shared running
+  // max, so tiles below the launch's max so far skip the exact dot; the
+  // per-slot values are then lower bounds only.  Null: per-pair maxima.
+  unsigned long long* maxrho_all;
   double* grid;                   // per output slot: lx x ly knot grid, or null
   double* diag;                   // per output slot: K at tiles (i, i), or null
   unsigned long long grid_stride, diag_stride;
@@ -181,15 +186,23 @@ __host__ __device__ constexpr int ring_stride(int DP) { return DP <= 2 ? 2 : DP 
 // d = 9..16 (DP = 16): the top lane stores its alpha' straight to global
 // memory instead of parking a chunk of them in shared memory, which keeps the
 // per-warp stage under 1/12 of the SM's shared memory (12 warps resident)
+// Measured (cfg-5 shape, d = 16): parking the top lane's alpha' in shared
+// memory and handing it up per chunk beats per-step global stores (550 vs 560
+// ms per Gram of 64 members) once the delta stage is gone (inline deltas), so
+// every register kernel parks.
 #ifndef SK_DIRECT_OUT_MIN_DP
-#define SK_DIRECT_OUT_MIN_DP 16
+#define SK_DIRECT_OUT_MIN_DP 32
 #endif
 __host__ __device__ constexpr bool direct_top_out(int DP) { return DP >= SK_DIRECT_OUT_MIN_DP; }
-__host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP) {
+// the chunk's deltas are staged in shared memory only where they are formed
+// per chunk: the literal kernels (exact sequential dots); the register
+// kernels form each tile's product inside the step (d <= 16)
+__host__ __device__ constexpr bool chunk_deltas(int N, int DP, bool lit) { return DP > 0 && (N == 0 || lit); }
+__host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP, bool lit = false) {
   return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + 32 * rows_per_lane(N) * col_stride(N) +
          (direct_top_out(DP) ? 0 : chunk_cols(rows_per_lane(N)) * col_stride(N)) +
          (DP > 0 ? ring_rows(rows_per_lane(N)) * ring_stride(DP) : 0) +
-         (DP > 0 ? rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32 : 0);
+         (chunk_deltas(N, DP, lit) ? rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32 : 0);
 }
 
 // ---- large d (DP == 0): the increment products are produced INSIDE the
@@ -244,8 +257,8 @@ __host__ __device__ constexpr int sweep_warps(int N, int DP) { return DP == 0 ? 
 // bands swept concurrently by one CTA
 __host__ __device__ constexpr int band_workers(int N, int DP) { return DP == 0 ? rho_bands(N) : kSweepWarps; }
 // dynamic shared memory of one CTA (doubles)
-__host__ __device__ constexpr int sweep_smem_doubles(int N, int DP) {
-  return DP > 0 ? kSweepWarps * stage_doubles_per_warp(N, DP) : rho_bands(N) * rho_slot_doubles(N);
+__host__ __device__ constexpr int sweep_smem_doubles(int N, int DP, bool lit = false) {
+  return DP > 0 ? kSweepWarps * stage_doubles_per_warp(N, DP, lit) : rho_bands(N) * rho_slot_doubles(N);
 }
 
 // producer / consumer hand-shake of a DP == 0 band CTA (static shared memory)
@@ -400,7 +413,7 @@ __device__ __forceinline__ void sts_series(double* dst, const double (&v)[NA], i
 // waiting on the band below's progress counter.  Segment mode: one segment,
 // all inputs complete; `restore` loads the band's lane state from its record
 // (not the band's first segment), `save` stores it (not the last).
-template <int N, int DP, bool EXACT, bool EXTRAS>
+template <int N, int DP, bool EXACT, bool EXTRAS, bool LIT = false>
 __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsigned b, int lane,
                                           double* __restrict__ smem, int c_begin, int c_end, bool restore,
                                           bool save, RhoCtl* ctl) {
@@ -417,7 +430,20 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // increments products formed inside the step (not per chunk) where the
   // registers allow it: d <= 8, register kernels, no exact max.  Measured:
   // 256 x 4096^2 62.95 vs 63.5 ms; at d = 16 it spills and gains nothing.
-  constexpr bool kInlineDelta = SK_INLINE_DELTA && DP > 0 && DP <= 8 && N > 0 && !EXACT && R == 1;
+  // Register kernels form each tile's increment product inside the step (its
+  // loads and FMAs overlap the tile math's dependency chains); the EXACT
+  // variant tracks the lane's largest fast |delta| per chunk and re-forms the
+  // chunk's products with the sequential dot only when that could raise the
+  // exact max (chunk end).  Measured: 256 x 4096^2 at d = 16, 64.7 vs 69.9 ms
+  // against per-chunk products in shared memory.
+  constexpr bool kInlineDelta = SK_INLINE_DELTA && DP > 0 && N > 0 && !LIT && R == 1;
+  static_assert(kInlineDelta == (DP > 0 && !chunk_deltas(N, DP, LIT)) || !SK_INLINE_DELTA,
+                "shared-memory delta stage exactly where deltas are formed per chunk");
+  // LIT: the literal (bit-identical) arithmetic at a compile-time order N,
+  // unscaled series in registers (strict-corner re-sweeps); like N == 0 it
+  // needs the exact deltas and every total
+  static_assert(!LIT || (N > 0 && EXACT && EXTRAS), "LIT variants are <N > 0, EXACT, EXTRAS>");
+  constexpr bool kLiteral = N == 0 || LIT;
   double* s_alpha = smem;                                   // 2 x K x NP
   double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
   double* s_out = s_pass + 32 * R * NP;                     // K x NP
@@ -456,7 +482,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const unsigned out = P.pair_out[p];
   const bool strict = (P.flags & kFlagStrictCorner) != 0;
   const bool fault = (P.flags & kFlagWFault) != 0;
-  const bool all_totals = EXTRAS || N == 0 || (P.flags & kFlagAllTotals) != 0;
+  const bool all_totals = EXTRAS || kLiteral || (P.flags & kFlagAllTotals) != 0;
   const bool band_top = row0 + 32 * R >= rows;  // the band holds the pair's last row
   const bool streaming = P.seg_cols == 0;
   double* const rec = streaming ? nullptr
@@ -502,8 +528,13 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // running exact max|delta| of this band: start from the pair's value so far
   // (a valid lower bound) so fewer tiles need the exact dot
   double mx = 0.0;
-  if constexpr (EXACT && N > 0) {
+  double fmx[R];  // EXACT, inline products: the lane's largest fast |delta| in the chunk
+#pragma unroll
+  for (int r = 0; r < R; ++r) fmx[r] = 0.0;
+  if constexpr (EXACT && !kLiteral) {
     if (P.maxrho) mx = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.maxrho + out)));
+    if (P.maxrho_all)
+      mx = fmax(mx, __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(P.maxrho_all))));
   }
   unsigned jkey[R];  // (first failing column << 2) | code, per tile
 #pragma unroll
@@ -637,6 +668,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
         jkey[r] = min(jkey[r], (act && !(fabs(delta) <= kDeltaOverflowLimit))
                                    ? (static_cast<unsigned>(j) << 2) | kErrDelta
                                    : ~0u);
+        if constexpr (EXACT) fmx[r] = fmax(fmx[r], act ? fabs(delta) : 0.0);
       } else if constexpr (DP > 0) {
         delta = dl[(r * K + k) * 32 + lane];
       } else {
@@ -644,7 +676,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       }
       double qo[NA];
       double total = 0.0;
-      if constexpr (N > 0) {
+      if constexpr (LIT) {
+        total = tile_step_literal_reg<N>(q[r], r_in[r], delta, qo, ro_out[r], fault);
+      } else if constexpr (N > 0) {
         // the total (non-finite check, wavefront.cpp:169-173; the final
         // value) only in TOT chunks -- see kFlagAllTotals
         tile_update_scaled<N>(q[r], r_in[r], delta, qo, ro_out[r], fault);
@@ -672,12 +706,12 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       // the reference's throw order inside a tile: delta guard (checked when
       // the chunk's deltas are formed), corner check, non-finite total
       // (wavefront.cpp:150-173); the first failing tile of the row wins
-      const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0], N > 0 ? kCornerScreen : kCornerTol);
-      const bool nf = (TOT || N == 0) && !isfinite(total);
+      const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0], kLiteral ? kCornerTol : kCornerScreen);
+      const bool nf = (TOT || kLiteral) && !isfinite(total);
       const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
       const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
       jkey[r] = min(jkey[r], (active && code != 0u) ? kk : ~0u);
-      if (TOT || N == 0) st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
+      if (TOT || kLiteral) st_global_if(last_row[r] && j == cols - 1, P.values + out, total);
       if constexpr (EXTRAS) {
         if (P.grid)
           st_global_if(active,
@@ -716,7 +750,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if constexpr (EXACT && N == 0) {
+            if constexpr (EXACT && kLiteral) {
               dd[u] = exact_dot<DP>(dx[u], dy);  // the literal kernel repeats the reference bit for bit
             } else {
               double e0 = dx[u][0] * dy[0], e1 = dx[u][1] * dy[1];
@@ -741,12 +775,12 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           const int j = c0 + k - lane - 32 * r;
           const bool act = row_ok[r] && j >= 0 && j < cols && k < kend;
           const double ad = fabs(dd[u]);
-          if constexpr (EXACT && N == 0) mx = fmax(mx, act ? ad : 0.0);  // dd is exact here
-          if constexpr (EXACT && N > 0) cand |= (act && ad + P.dot_err >= mx) ? 1u << u : 0u;
+          if constexpr (EXACT && kLiteral) mx = fmax(mx, act ? ad : 0.0);  // dd is exact here
+          if constexpr (EXACT && !kLiteral) cand |= (act && ad + P.dot_err >= mx) ? 1u << u : 0u;
           const unsigned kk = (static_cast<unsigned>(j) << 2) | kErrDelta;
           jkey[r] = min(jkey[r], (act && !(ad <= kDeltaOverflowLimit)) ? kk : ~0u);
         }
-        if constexpr (EXACT && N > 0) {
+        if constexpr (EXACT && !kLiteral) {
           // exact max|delta| (bit-identical to max_abs_rho) without an exact
           // dot per tile: |fast - sequential| <= dot_err, so only a tile whose
           // fast |delta| + dot_err reaches the running exact max can raise it
@@ -874,13 +908,39 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       }
     };
     // totals where the pair's final tile can fall (or everywhere, kFlagAllTotals)
-    if constexpr (EXTRAS || N == 0) {
+    if constexpr (EXTRAS || kLiteral) {
       run_chunk(true);
     } else {
       if (all_totals || (band_top && c0 + K > cols - 1))
         run_chunk(true);
       else
         run_chunk(false);
+    }
+    if constexpr (EXACT && kInlineDelta) {
+      // exact max|delta| (bit-identical to max_abs_rho): |fast - sequential|
+      // <= dot_err, so only a lane whose largest fast |delta| of the chunk
+      // plus dot_err reaches the running exact max can raise it -- rare once
+      // the max has settled; that lane re-forms its chunk's products with the
+      // sequential dot from the dx ring (the chunk's rows are still there: the
+      // next chunk's staging fills rows 16 to 31 columns ahead of lane 31)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool cand = fmx[r] + P.dot_err >= mx;
+        if (__any_sync(0xffffffffu, cand) && cand) {
+#pragma unroll 1
+          for (int k = 0; k < kend; ++k) {
+            const int j = c0 + k - lane - 32 * r;
+            if (row_ok[r] && j >= 0 && j < cols) {
+              const double* xr = s_ring + (j & (RING - 1)) * XS;
+              double row[DP > 0 ? DP : 1];
+#pragma unroll
+              for (int c = 0; c < DP; ++c) row[c] = xr[c];
+              mx = fmax(mx, fabs(exact_dot<DP>(row, dyr[r])));
+            }
+          }
+        }
+        fmx[r] = 0.0;
+      }
     }
     hand_up(c0, kend);
     if (DP == 0 && !tab_mode) {
@@ -914,8 +974,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     if (P.maxrho) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0 && mx > 0.0)
+      if (lane == 0 && mx > 0.0) {
         atomicMax(P.maxrho + out, static_cast<unsigned long long>(__double_as_longlong(mx)));
+        if (P.maxrho_all) atomicMax(P.maxrho_all, static_cast<unsigned long long>(__double_as_longlong(mx)));
+      }
     }
   }
   return kBandDone;
@@ -1075,8 +1137,8 @@ __device__ __forceinline__ void rho_producer(const SweepParams& P, double* __res
 // sweep_smem_doubles(N, DP) doubles.  DP == 0: warps 0..B-1 sweep B bands,
 // warps B..2B-1 produce their rho (band slot k: sweep warp k, producer warp
 // B + k, named barriers 1 + 2k / 2 + 2k), B = rho_bands(N).
-template <int N, int DP, bool EXACT, bool EXTRAS>
-__global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 ? 1 : sweep_min_blocks(N))
+template <int N, int DP, bool EXACT, bool EXTRAS, bool LIT = false>
+__global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 || LIT ? 1 : sweep_min_blocks(N))
     sweep_kernel(const SweepParams P) {
   constexpr int kBands = DP == 0 ? rho_bands(N) : 1;
   static_assert(DP > 0 || kBands >= 1, "a band's shared memory must fit the SM");
@@ -1087,12 +1149,12 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 ? 1 : sweep_m
   const int kslot = DP == 0 ? warp % kBands : 0;
   RhoCtl& s_ctl = s_ctls[kslot];
   const unsigned bar_start = 1u + 2u * kslot, bar_end = 2u + 2u * kslot;
-  double* smem = DP == 0 ? s_dyn + kslot * rho_slot_doubles(N) : s_dyn + warp * stage_doubles_per_warp(N, DP);
+  double* smem = DP == 0 ? s_dyn + kslot * rho_slot_doubles(N) : s_dyn + warp * stage_doubles_per_warp(N, DP, LIT);
   if constexpr (DP == 0) {
     if (warp >= kBands) {
       if (P.rho_tab != nullptr) return;  // table mode: no producers
       double* ring = smem + stage_doubles_per_warp(N, 0);
-      rho_producer<N == 0>(P, ring, ring + rho_ring_doubles(), &s_ctl, lane, bar_start, bar_end);
+      rho_producer<N == 0 || LIT>(P, ring, ring + rho_ring_doubles(), &s_ctl, lane, bar_start, bar_end);
       return;
     }
   }
@@ -1118,7 +1180,7 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 ? 1 : sweep_m
       }
       named_bar_sync(bar_start, 64);
     }
-    const int st = sweep_band<N, DP, EXACT, EXTRAS>(P, p, b, lane, smem, c_begin, c_end, restore, save, &s_ctl);
+    const int st = sweep_band<N, DP, EXACT, EXTRAS, LIT>(P, p, b, lane, smem, c_begin, c_end, restore, save, &s_ctl);
     if (with_producer) {
       if (st == kBandAbort && lane == 0) *reinterpret_cast<volatile unsigned*>(&s_ctl.abort) = 1u;
       named_bar_sync(bar_end, 64);

@@ -9,9 +9,10 @@
 namespace skb {
 
 #define SK_DECL(n)                                                                                          \
-  __attribute__((weak)) cudaError_t sweep_launch_n##n(int dp, bool exact, bool extras, int grid,           \
+  __attribute__((weak)) cudaError_t sweep_launch_n##n(int dp, bool exact, bool extras, bool literal, int grid, \
                                                       cudaStream_t stream, const SweepParams& P);           \
-  __attribute__((weak)) cudaError_t sweep_occupancy_n##n(int dp, bool exact, bool extras, int* blocks_per_sm);
+  __attribute__((weak)) cudaError_t sweep_occupancy_n##n(int dp, bool exact, bool extras, bool literal,      \
+                                                         int* blocks_per_sm);
 SK_DECL(0) SK_DECL(1) SK_DECL(2) SK_DECL(3) SK_DECL(4) SK_DECL(5) SK_DECL(6) SK_DECL(7) SK_DECL(8)
 SK_DECL(9) SK_DECL(10) SK_DECL(11) SK_DECL(12) SK_DECL(13) SK_DECL(14) SK_DECL(15) SK_DECL(16)
 #undef SK_DECL
@@ -26,17 +27,17 @@ SK_DECL(9) SK_DECL(10) SK_DECL(11) SK_DECL(12) SK_DECL(13) SK_DECL(14) SK_DECL(1
   SK_CASE(12, fn, __VA_ARGS__) SK_CASE(13, fn, __VA_ARGS__) SK_CASE(14, fn, __VA_ARGS__)                   \
   SK_CASE(15, fn, __VA_ARGS__) SK_CASE(16, fn, __VA_ARGS__)
 
-cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, int grid, cudaStream_t stream,
+cudaError_t sweep_launch(int n_template, int dp, bool exact, bool extras, bool literal, int grid, cudaStream_t stream,
                          const SweepParams& P) {
   switch (n_template) {
-    SK_ALL(sweep_launch_n, dp, exact, extras, grid, stream, P)
+    SK_ALL(sweep_launch_n, dp, exact, extras, literal, grid, stream, P)
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, int* blocks_per_sm) {
+cudaError_t sweep_occupancy(int n_template, int dp, bool exact, bool extras, bool literal, int* blocks_per_sm) {
   switch (n_template) {
-    SK_ALL(sweep_occupancy_n, dp, exact, extras, blocks_per_sm)
+    SK_ALL(sweep_occupancy_n, dp, exact, extras, literal, blocks_per_sm)
     default: return cudaErrorInvalidValue;
   }
 }

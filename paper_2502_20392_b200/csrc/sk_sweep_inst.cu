@@ -15,12 +15,12 @@
 
 namespace skb {
 
-template <int N, int DP, bool EXACT, bool EXTRAS>
+template <int N, int DP, bool EXACT, bool EXTRAS, bool LIT = false>
 static size_t smem_bytes() {
-  return static_cast<size_t>(sweep_smem_doubles(N, DP)) * sizeof(double);
+  return static_cast<size_t>(sweep_smem_doubles(N, DP, LIT)) * sizeof(double);
 }
 
-template <int N, int DP, bool EXACT, bool EXTRAS>
+template <int N, int DP, bool EXACT, bool EXTRAS, bool LIT = false>
 static cudaError_t prepare() {
   // function attributes are per device: set them once per device
   static std::atomic<unsigned long long> done_mask{0};
@@ -29,24 +29,24 @@ static cudaError_t prepare() {
   if (e != cudaSuccess) return e;
   const unsigned long long bit = 1ull << (dev & 63);
   if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
-  const size_t smem = smem_bytes<N, DP, EXACT, EXTRAS>();
+  const size_t smem = smem_bytes<N, DP, EXACT, EXTRAS, LIT>();
   if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS, LIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   // the whole unified L1/shared array as shared memory: residency is set by
   // registers and the per-warp stage, never by a smaller default carveout
   // (the sweep reads global memory only through L2-bypassing cp.async)
-  e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  e = cudaFuncSetAttribute(sweep_kernel<N, DP, EXACT, EXTRAS, LIT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_acq_rel);
   return e;
 }
 
-template <int N, int DP, bool EXACT, bool EXTRAS>
+template <int N, int DP, bool EXACT, bool EXTRAS, bool LIT = false>
 static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& P) {
-  cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
+  cudaError_t e = prepare<N, DP, EXACT, EXTRAS, LIT>();
   if (e != cudaSuccess) return e;
 #ifdef SK_PROFILE_WAITS
   {
@@ -57,7 +57,7 @@ static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& 
     cudaMemsetAsync(tp, 0, kTraceUnits * 4 * sizeof(unsigned long long), stream);
   }
 #endif
-  sweep_kernel<N, DP, EXACT, EXTRAS><<<grid, sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS>(), stream>>>(P);
+  sweep_kernel<N, DP, EXACT, EXTRAS, LIT><<<grid, sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS, LIT>(), stream>>>(P);
 #ifdef SK_PROFILE_WAITS
   if (const char* path = std::getenv("SK_UTRACE")) {
     static std::vector<unsigned long long> h(kTraceUnits * 4);
@@ -72,12 +72,12 @@ static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& 
   return cudaGetLastError();
 }
 
-template <int N, int DP, bool EXACT, bool EXTRAS>
+template <int N, int DP, bool EXACT, bool EXTRAS, bool LIT = false>
 static cudaError_t occupancy_one(int* blocks_per_sm) {
-  cudaError_t e = prepare<N, DP, EXACT, EXTRAS>();
+  cudaError_t e = prepare<N, DP, EXACT, EXTRAS, LIT>();
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<N, DP, EXACT, EXTRAS>,
-                                                       sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS>());
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, sweep_kernel<N, DP, EXACT, EXTRAS, LIT>,
+                                                       sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS, LIT>());
 }
 
 #define SK_CAT2(a, b) a##b
@@ -104,12 +104,31 @@ static cudaError_t occupancy_one(int* blocks_per_sm) {
     default: return cudaErrorInvalidValue;       \
   }
 
-cudaError_t SK_CAT(sweep_launch_n, SK_N)(int dp, bool exact, bool extras, int grid, cudaStream_t stream,
+// Literal arithmetic at this compile-time order (strict-corner re-sweeps of
+// register-kernel pairs): instantiated for the order every Brownian config
+// runs at (N = 8); other orders re-sweep with the runtime-order kernel N = 0.
+#if SK_N == 8
+#define SK_LIT_SWITCH(FN, ...)                                           \
+  switch (dp) {                                                          \
+    case 0: return FN<SK_N, 0, true, true, true>(__VA_ARGS__);           \
+    case 2: return FN<SK_N, 2, true, true, true>(__VA_ARGS__);           \
+    case 4: return FN<SK_N, 4, true, true, true>(__VA_ARGS__);           \
+    case 8: return FN<SK_N, 8, true, true, true>(__VA_ARGS__);           \
+    case 16: return FN<SK_N, 16, true, true, true>(__VA_ARGS__);         \
+    default: return cudaErrorInvalidValue;                               \
+  }
+#else
+#define SK_LIT_SWITCH(FN, ...) return cudaErrorInvalidValue;
+#endif
+
+cudaError_t SK_CAT(sweep_launch_n, SK_N)(int dp, bool exact, bool extras, bool literal, int grid, cudaStream_t stream,
                                          const SweepParams& P) {
+  if (literal) SK_LIT_SWITCH(launch_one, grid, stream, P)
   SK_DP_SWITCH(launch_one, grid, stream, P)
 }
 
-cudaError_t SK_CAT(sweep_occupancy_n, SK_N)(int dp, bool exact, bool extras, int* blocks_per_sm) {
+cudaError_t SK_CAT(sweep_occupancy_n, SK_N)(int dp, bool exact, bool extras, bool literal, int* blocks_per_sm) {
+  if (literal) SK_LIT_SWITCH(occupancy_one, blocks_per_sm)
   SK_DP_SWITCH(occupancy_one, blocks_per_sm)
 }
 

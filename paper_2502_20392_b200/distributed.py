@@ -109,7 +109,7 @@ def gram_matrix_distributed(family: Sequence, options: Optional[sk.GramOptions] 
     r.min_order = int(computed.min()) if computed.size else 0
     r.max_order = int(computed.max()) if computed.size else 0
     r.max_abs_increment_product = float(stats[0].item())
-    r.pair_max_abs_rho = out[2].ravel()
+    r.pair_max_abs_rho = out[2].ravel() if local.pair_max_abs_rho is not None else None
     n_ok = int(np.sum(~np.isnan(r.values)))
     r.peak_live_series = sk._peak_live(length - 1, length - 1) if n_ok else 0
     if options.compute_bound:

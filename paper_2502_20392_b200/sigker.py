@@ -454,6 +454,10 @@ class GramOptions:
     # GPUs to spread this call over, one host thread each (a sub-shard per
     # device); empty: the current device
     devices: List[int] = field(default_factory=list)
+    # also return every entry's exact max|rho| (GramResult.pair_max_abs_rho);
+    # without it only the family's maximum is formed (cheaper: one running
+    # max for the whole launch lets most tiles skip the exact dot)
+    pair_max_abs_rho: bool = False
 
 
 @dataclass
@@ -560,8 +564,8 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
         nf = ctypes.c_size_t()
         rc = lib.sk_gram(_ptr(padded), m, max_len, dim, 1 if adaptive else 0, int(options.policy.order),
                          float(options.policy.tol), flags, 1 if scan else 0, int(sub), int(nsub), _ptr(vals),
-                         _ptr(ords), _ptr(pm), ctypes.byref(mp), ctypes.byref(cv), ctypes.byref(nf),
-                         ctypes.byref(status))
+                         _ptr(ords), _ptr(pm) if options.pair_max_abs_rho else None, ctypes.byref(mp),
+                         ctypes.byref(cv), ctypes.byref(nf), ctypes.byref(status))
         return rc, (_gram_failures(lib, nf.value) if rc == 0 else [])
 
     devices = list(options.devices)
@@ -622,7 +626,7 @@ def gram_matrix(family: Sequence, options: Optional[GramOptions] = None, shard: 
     r.peak_live_series = _peak_live(max_len - 1, max_len - 1) if n_ok else 0
     if scan:
         r.max_abs_increment_product = float(maxp.value)
-        r.pair_max_abs_rho = pmax
+        r.pair_max_abs_rho = pmax if options.pair_max_abs_rho else None
     if options.compute_bound:
         r.bound = gram_error_bound(ErrorBoundInputs(m, max_len, r.max_abs_increment_product, r.min_order))
     return r

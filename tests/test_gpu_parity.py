@@ -638,3 +638,57 @@ def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
     v_ref, _ = restatement.propagate(x1, y1, 20)
     assert sk.propagate(x1, y1, 20).value == v_ref
     assert rel(sk.propagate(x1, y1, 8).value, restatement.propagate(x1, y1, 8)[0]) < TOL
+
+
+@pytest.mark.parametrize("kernel", ["register", "runtime"])
+def test_literal_kernels_bit_identical_to_the_reference(sk, restatement, monkeypatch, kernel):
+    """The literal kernels -- the order-8 register-resident one the strict
+    re-sweeps use, and the runtime-order one -- repeat the reference's
+    arithmetic bit for bit (values, knot grids, max|rho|) across the delta
+    paths (inline d <= 8, per-chunk d = 9..16, large d through the producer
+    ring and the table)."""
+    monkeypatch.setenv("SK_FORCE_LITERAL", "1")
+    if kernel == "runtime":
+        monkeypatch.setenv("SK_NO_LIT_REG", "1")
+    rng = restatement.rng(8088)
+    for d in (1, 2, 5, 8, 13, 16, 40):
+        x = rng.random_series(70, d, 1.0)
+        y = rng.random_series(90, d, 1.0)
+        v_ref, _, g_ref = restatement.propagate(x, y, 8, grid=True)
+        assert sk.propagate(x, y, 8).value == v_ref, d
+        g = sk.propagate_grid(x, y, 8)
+        assert np.asarray(g.grid).tolist() == g_ref.tolist(), d
+        res = sk.pairwise(np.stack([x, x]), np.stack([y, y[::-1].copy()]), sk.TruncationPolicy.fixed(8),
+                          want_max_abs_rho=True)
+        assert res.values[0] == v_ref
+        assert res.values[1] == restatement.propagate(x, y[::-1].copy(), 8)[0]
+        assert res.max_abs_rho[0] == restatement.max_abs_rho(x, y)
+        if d == 40:
+            monkeypatch.setenv("SK_RHO_FUSED", "1")
+            assert sk.propagate(x, y, 8).value == v_ref
+            monkeypatch.delenv("SK_RHO_FUSED")
+
+
+def test_gram_max_product_with_and_without_per_pair_maxima(sk, restatement):
+    """GramResult.max_abs_increment_product (gram.cpp:89-96) is the exact
+    maximum over the family whether or not the per-entry maxima are asked for
+    (without them one launch-wide running max lets tiles skip the exact dot);
+    with them every entry is its pair's exact max|rho|."""
+    fam = [restatement.brownian(300 + 7 * k, 16, 90 + k) for k in range(6)]
+    fam[3] = fam[3] * 2.5
+    pol = sk.TruncationPolicy.adaptive(1e-12)
+    a = sk.gram_matrix(fam, sk.GramOptions(policy=pol))
+    b = sk.gram_matrix(fam, sk.GramOptions(policy=pol, pair_max_abs_rho=True))
+    assert a.pair_max_abs_rho is None
+    assert a.max_abs_increment_product == b.max_abs_increment_product
+    assert np.asarray(a.values).tobytes() == np.asarray(b.values).tobytes()
+    L = max(s.shape[0] for s in fam)
+    padded = [np.concatenate([s, np.repeat(s[-1:], L - s.shape[0], axis=0)]) for s in fam]
+    P = np.asarray(b.pair_max_abs_rho).reshape(6, 6)
+    best = 0.0
+    for i in range(6):
+        for j in range(i, 6):
+            mr = restatement.max_abs_rho(padded[i], padded[j])
+            assert P[i, j] == mr and P[j, i] == mr
+            best = max(best, mr)
+    assert a.max_abs_increment_product == best
