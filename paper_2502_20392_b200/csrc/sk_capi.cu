@@ -909,8 +909,8 @@ int pairwise_core(Ctx& c, const double* d_xraw, size_t lx, const double* d_yraw,
   SK_CUDA(cudaStreamSynchronize(c.stream()));
   SK_CUDA(cudaGetLastError());
   tr.mark("sweep done (sync)");
-  // grid / diagonal sweeps form every total already
-  if (int rc = recheck_failures(c, ps, px, py, res.orders, flags, o, hv, res.err, d_grid || d_diag, st)) return rc;
+  // knot-grid sweeps form every total already (the diagonal only near tiles (i, i))
+  if (int rc = recheck_failures(c, ps, px, py, res.orders, flags, o, hv, res.err, d_grid != nullptr, st)) return rc;
   return SK_OK;
 }
 

@@ -482,7 +482,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const unsigned out = P.pair_out[p];
   const bool strict = (P.flags & kFlagStrictCorner) != 0;
   const bool fault = (P.flags & kFlagWFault) != 0;
-  const bool all_totals = EXTRAS || kLiteral || (P.flags & kFlagAllTotals) != 0;
+  // every tile's total: literal kernels, the re-sweep flag, knot grids; the
+  // knot diagonal needs them only in the chunks holding a tile (i, i)
+  const bool all_totals = kLiteral || (P.flags & kFlagAllTotals) != 0 || (EXTRAS && P.grid != nullptr);
   const bool band_top = row0 + 32 * R >= rows;  // the band holds the pair's last row
   const bool streaming = P.seg_cols == 0;
   double* const rec = streaming ? nullptr
@@ -908,10 +910,12 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       }
     };
     // totals where the pair's final tile can fall (or everywhere, kFlagAllTotals)
-    if constexpr (EXTRAS || kLiteral) {
+    if constexpr (kLiteral) {
       run_chunk(true);
     } else {
-      if (all_totals || (band_top && c0 + K > cols - 1))
+      // lane t meets its diagonal tile (row0 + t, row0 + t) at step row0 + 2t
+      const bool diag_chunk = EXTRAS && P.diag != nullptr && c0 <= row0 + 62 && c0 + K > row0;
+      if (all_totals || diag_chunk || (band_top && c0 + K > cols - 1))
         run_chunk(true);
       else
         run_chunk(false);
