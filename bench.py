@@ -7,17 +7,20 @@ reference's own generator, bit for bit), adaptive truncation tol 1e-12
 (=> N = 8), as gram_matrix (gram.cpp:16-98) evaluates it: 524,800 upper-
 triangle kernel-evals of 4095^2 tile-updates each, plus each pair's exact
 max|rho| (GramResult.max_abs_increment_product).  One step = one of the
-32 equal slices of the upper-triangle pair range (16,400 kernel-evals,
-2.75e11 tile-updates); step s evaluates slice s mod 32, so 32 steps are the
-whole Gram.  With --gpus N the slice is split over N ranks (sk_gram_shard_
-range arithmetic: rank r owns sub-range s*N + r of 32*N) and assembled by an
-NCCL all-reduce of the m x m matrix inside the timed region: strong scaling.
+16 equal slices of the upper-triangle pair range (32,800 kernel-evals,
+5.5e11 tile-updates; large enough that a launch's tail -- the last pairs'
+critical path -- stays a few percent at 8 GPUs); step s evaluates slice
+s mod 16, so 16 steps are the whole Gram.  With --gpus N the slice is split
+over N ranks (sk_gram_shard_range arithmetic: rank r owns sub-range s*N + r
+of 16*N) and assembled by an NCCL all-reduce of the m x m matrix inside the
+timed region: strong scaling.
 
   value : kernel-evals/s of the whole job, family resident in HBM on every
           rank (sk_gram_device into a device matrix + all-reduce)
   e2e   : the same through the public API (distributed.gram_matrix_
           distributed -> sk_gram): every step copies the pinned host family
-          to the device and reads the matrix back
+          to the device and reads the matrix back (min(K, 4) timed steps:
+          the same metric over a shorter run)
   roofline : the dominant kernel (skb::sweep_kernel<8,16,EXACT>): algorithmic
           FP64 flops F(N,d) = 4(N+1)^2 + 2d per tile-update over its
           CUDA-event time (library event pair on the launching stream),
@@ -51,7 +54,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 M, LEN, DIM, SEED0, TOL = 1024, 4096, 16, 1000, 1e-12
-SLICES = 32
+SLICES = 16
 ORDER = 8
 FP64_PEAK_TFLOPS = 37.11  # measured: tools/fp64_peak.cu DMMA m8n8k4 (DFMA 34.2); profiles/fp64_peak_r01.txt
 CPU_SAMPLE_PAIRS = 16
@@ -153,7 +156,7 @@ def free_port():
 def relaunch(args):
     """--gpus N outside torchrun: run this script under torch.distributed.run
     with N ranks (one per GPU) and pass its exit code through."""
-    if not args.cpu_smoke:
+    if not args.cpu_smoke and not args.share_gpu:
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -368,6 +371,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip BASELINE configs 1-4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-smoke", action="store_true", help="gloo CPU run of the multi-rank plumbing")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: all ranks on cuda:0 over gloo (the multi-rank GPU path on a 1-GPU box; "
+                         "the Gram shards are independent, so sharing one GPU cannot deadlock)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -383,14 +389,27 @@ def main():
     import ctypes
     import torch
     dist = None
-    if torch.cuda.device_count() < max(1, ws):
+    if args.share_gpu:
+        local = 0
+    elif torch.cuda.device_count() < max(1, ws):
         print(f"bench.py: {ws} rank(s) but {torch.cuda.device_count()} GPU(s) visible", file=sys.stderr)
         return 1
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+
+    def allreduce_(t, op):
+        if args.share_gpu:  # gloo: through host memory
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op)
 
     from paper_2502_20392_b200 import _capi
     from paper_2502_20392_b200 import sigker as sk
@@ -423,7 +442,7 @@ def main():
         if rc != 0:
             raise RuntimeError(st.message.decode())
         if dist is not None:
-            dist.all_reduce(mat, op=dist.ReduceOp.SUM)
+            allreduce_(mat, dist.ReduceOp.SUM)
         return mat
 
     def barrier():
@@ -444,7 +463,7 @@ def main():
         ms = e0.elapsed_time(e1)
         if dist is not None:
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            allreduce_(t, dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
 
@@ -480,12 +499,14 @@ def main():
         def e2e_step(step):
             s = step % SLICES
             if dist is not None:
-                skd.gram_matrix_distributed(fam_h, opts, shard=s, nshards=SLICES)
+                skd.gram_matrix_distributed(fam_h, opts, shard=s, nshards=SLICES,
+                                            device=torch.device("cpu") if args.share_gpu else None)
             else:
                 sk.gram_matrix(fam_h, opts, shard=s, nshards=SLICES)
         e2e_step(SLICES - 1)
-        ms_e2e = timed(e2e_step, args.steps, 0)
-    e2e_value = pairs_per_step / (ms_e2e / args.steps / 1e3) if ms_e2e else None
+        e2e_steps = min(args.steps, 4)
+        ms_e2e = timed(e2e_step, e2e_steps, 0)
+    e2e_value = pairs_per_step / (ms_e2e / e2e_steps / 1e3) if ms_e2e else None
 
     # roofline of the dominant kernel (this rank's launches)
     avg_launch_ms = stats["sweep_ms"] / max(1, stats["sweep_launches"])

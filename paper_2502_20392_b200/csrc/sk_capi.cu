@@ -502,8 +502,21 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     const double work_steps = pairs_launch * bands * (cols + 31.0) / warps_est;
     const bool force = std::getenv("SK_FORCE_SEGMENTS") != nullptr;
     // measured (N = 8): 256 pairs x 4096^2 best at L = 256/128; one pair of
-    // 262144^2 best at 64 (57 % vs 47 % streaming), of 10^6 at 128
+    // 262144^2 best at 64 (57 % vs 47 % streaming).  One pair alone: the
+    // largest L whose waves still hold a unit per warp and whose critical
+    // path fits in the work -- 10^6^2: L = 512, 13.97 s vs 15.2-15.6 s at 128
+    // (256: 17.5, 1024: 17.2; two runs each, round 2)
+    if (pairs_launch == 1.0 && !force) {
+      for (int L : {512, 256, 128, 64}) {
+        const double S = std::ceil((cols + 31.0) / L);
+        if (std::min<double>(bands, S) >= warps_est && (bands + S) * L <= work_steps) {
+          seg_cols = L;
+          break;
+        }
+      }
+    }
     for (const double crit_frac : {0.5, 1.0}) {
+      if (seg_cols) break;
       for (int L : {256, 128, 64}) {
         const double S = std::ceil((cols + 31.0) / L);
         if (force ||

@@ -155,3 +155,21 @@ def test_ipc_exchange_buffers_round_trip(sk):
         assert ctr[0] == 0
     finally:
         lib.sk_exchange_free(a, p)
+
+
+def test_bench_multi_rank_gpu_path_on_one_gpu():
+    """bench.py's N-rank GPU path -- sk_gram_device per rank on its share of
+    each slice, all-reduce assembly, max-over-ranks timing, parity of the
+    assembled slice against the reference's goldens -- with two ranks sharing
+    the box's one GPU over gloo (--share-gpu; the shards never wait on each
+    other)."""
+    import json
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--share-gpu", "--steps", "1",
+                          "--warmup", "1", "--no-extras", "--no-cpu-baseline", "--no-e2e"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["parity"]["golden_entries_checked"] >= 1
+    assert line["parity"]["max_rel_err"] <= 1e-10
