@@ -348,3 +348,37 @@ def test_bench_refuses_more_gpus_than_visible():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64"], capture_output=True,
                          text=True, timeout=300, cwd=ROOT)
     assert out.returncode != 0 and "GPU(s) visible" in out.stderr
+
+
+def test_block_cyclic_kernel_indexing_model():
+    """The sweep kernel's strip indexing (sk_sweep.cuh: unit -> band decode,
+    column-buffer slot, exchange-area rounds), restated in Python: every band
+    is swept by exactly one GPU, in increasing order on that GPU; a GPU's
+    concurrently live blocks never share a column buffer; and at every block
+    boundary the producer writes exactly the exchange slot its consumer reads,
+    in the consumer GPU's area."""
+    from paper_2502_20392_b200.distributed import strip_plan
+    for ly, G, S in ((400, 2, 3), (400, 3, 1), (1_000_001, 8, 1302), (999, 4, 7), (33, 1, 1)):
+        bands = (ly - 1 + 31) // 32
+        nblocks = -(-bands // S)
+        if nblocks < G:
+            continue
+        seen = []
+        for g in range(G):
+            owned, rounds, in_rounds = strip_plan(ly, 8, G, g, S)
+            decoded = []
+            for bi in range(owned):  # sweep_kernel streaming decode
+                b = (g + G * (bi // S)) * S + bi % S
+                decoded.append(b)
+                blk = b // S
+                assert blk % G == g and b < bands
+                assert blk // G < rounds  # column-buffer slot (round) exists
+                if b > 0 and b % S == 0:  # bottom band of a block: reads this GPU's area
+                    assert blk // G < in_rounds
+                if b + 1 < bands and (b + 1) % S == 0:  # top band: writes GPU (blk+1) mod G's area
+                    consumer = (blk + 1) % G
+                    _, _, c_in = strip_plan(ly, 8, G, consumer, S)
+                    assert (blk + 1) // G < c_in
+            assert decoded == sorted(decoded)
+            seen += decoded
+        assert sorted(seen) == list(range(bands))
