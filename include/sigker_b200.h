@@ -186,11 +186,13 @@ int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, s
                        uint32_t flags, size_t gpus, size_t rank, size_t block, const void* in_abuf,
                        const void* in_prog, void* out_abuf, void* out_prog, double* value, double* diag,
                        sk_status* st);
-/* One-GPU emulation of the whole pipeline in a single launch: every `block`
- * bands the hand-off goes through an exchange area with the multi-GPU
- * protocol.  Test entry point. */
+/* One-GPU emulation of the whole pipeline of `gpus` GPUs in a single launch
+ * (every band, global order; column buffers and exchange areas per virtual
+ * GPU; every `block` bands the hand-off goes through an exchange area with the
+ * multi-GPU protocol, the last virtual GPU handing to the first).  Test entry
+ * point. */
 int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order,
-                       uint32_t flags, size_t block, double* value, sk_status* st);
+                       uint32_t flags, size_t gpus, size_t block, double* value, sk_status* st);
 
 /* Device-time accounting of the sweep kernels on the calling thread
  * (CUDA events around every sweep launch). */

@@ -105,7 +105,7 @@ def load():
         "sk_enable_peer_access": ([ctypes.c_int, ST], ctypes.c_int),
         "sk_propagate_strip": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, SZ, SZ, P, P, P, P, P, P, ST],
                                ctypes.c_int),
-        "sk_propagate_split": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, P, ST], ctypes.c_int),
+        "sk_propagate_split": ([P, SZ, P, SZ, SZ, ctypes.c_int, ctypes.c_uint32, SZ, SZ, P, ST], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -382,6 +382,7 @@ int check_watchdog(Ctx& c, sk_status* st) {
 struct Strip {
   int gpus = 1, rank = 0, block = 0;  // block = 0: all bands in one block
   bool exch = false;
+  bool emul = false;  // one launch over all `gpus` virtual GPUs (sk_propagate_split)
   const double* xin_abuf = nullptr;
   const unsigned long long* xin_prog = nullptr;
   double* xout_abuf = nullptr;
@@ -491,8 +492,13 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   // strips).
   const bool whole = strip.gpus == 1 && !strip.exch;
   const size_t sblock = strip.block > 0 ? static_cast<size_t>(strip.block) : static_cast<size_t>(bands);
-  const StripPlan plan = strip_plan(static_cast<size_t>(bands), static_cast<size_t>(strip.gpus),
-                                    static_cast<size_t>(strip.rank), sblock);
+  StripPlan plan = strip_plan(static_cast<size_t>(bands), static_cast<size_t>(strip.gpus),
+                              static_cast<size_t>(strip.rank), sblock);
+  const size_t xrounds = (((bands + sblock - 1) / sblock) + strip.gpus - 1) / strip.gpus;
+  if (strip.emul) {
+    plan.owned_bands = static_cast<size_t>(bands);
+    plan.rounds = static_cast<size_t>(strip.gpus) * xrounds;
+  }
   int seg_cols = 0;
   unsigned spb = 0, units_pair = 0;
   if (bands > 1 && whole && std::getenv("SK_STREAM") == nullptr) {
@@ -660,6 +666,8 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.xrank = strip.rank;
     P.xblock = static_cast<int>(sblock);
     P.xexch = strip.exch ? 1 : 0;
+    P.xemul = strip.emul ? 1 : 0;
+    P.xrounds = static_cast<int>(xrounds);
     P.units_pair_streaming = nb;
     P.xin_abuf = strip.xin_abuf;
     P.xin_prog = strip.xin_prog;
@@ -1572,28 +1580,31 @@ int sk_propagate_strip(const double* x, size_t lx, const double* y, size_t ly, s
   return SK_OK;
 }
 
-// One-GPU emulation of the strip pipeline: ONE launch sweeps every band, but
-// every `block` bands the hand-off goes through an exchange area with
-// system-scope release/acquire, exactly as between GPUs.  Used to test the
-// strip path on one GPU (strips on one GPU may not run as separate launches
-// that wait on each other).
+// One-GPU emulation of the strip pipeline: ONE launch sweeps every band of
+// all `gpus` virtual GPUs (global band order), with the block-cyclic layout's
+// column buffers and exchange areas per virtual GPU and every block boundary
+// handed over through an exchange area with system-scope release/acquire,
+// exactly as between GPUs.  Used to test the multi-GPU path on one GPU
+// (strips on one GPU may not run as separate launches that wait on each other).
 int sk_propagate_split(const double* x, size_t lx, const double* y, size_t ly, size_t dim, int order, uint32_t flags,
-                       size_t block, double* value, sk_status* st) {
+                       size_t gpus, size_t block, double* value, sk_status* st) {
   clear_status(st);
   size_t bands = 0;
-  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2 || block < 1 || block >= bands)
-    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_split: block outside [1, bands)");
+  if (dim < 1 || sk_strip_bands(ly, order, &bands) != SK_OK || lx < 2 || block < 1 || block >= bands || gpus < 1)
+    return set_status(st, SK_INVALID_ARGUMENT, 0, 0, "propagate_split: block outside [1, bands) or no GPUs");
   const size_t nblocks = (bands + block - 1) / block;
+  const size_t xrounds = (nblocks + gpus - 1) / gpus;
   void *xa = nullptr, *xp = nullptr;
-  if (int rc = sk_exchange_alloc(lx, order, nblocks, &xa, &xp, st)) return rc;
+  if (int rc = sk_exchange_alloc(lx, order, gpus * xrounds, &xa, &xp, st)) return rc;
   Ctx* cp = nullptr;
   int rc = get_ctx(&cp, st);
   if (rc == SK_OK) {
     Strip s;
-    s.gpus = 1;
+    s.gpus = static_cast<int>(gpus);
     s.rank = 0;
     s.block = static_cast<int>(block);
     s.exch = true;
+    s.emul = true;
     s.xin_abuf = static_cast<const double*>(xa);
     s.xout_abuf = static_cast<double*>(xa);
     s.xin_prog = static_cast<const unsigned long long*>(xp);

@@ -119,7 +119,10 @@ struct SweepParams {
   // writes xout_abuf[r'] / publishes xout_prog[r'] (the next GPU's exchange
   // area, peer memory; r' = (k + 1) / xgpus), system-scope release/acquire.
   // One GPU, one launch: xgpus = 1, xblock = bands, xexch = 0.
-  int xgpus, xrank, xblock, xexch;
+  // xemul: ONE launch sweeps every band of all xgpus virtual GPUs (global band
+  // order; the test of the multi-GPU indexing on one GPU): GPU g's round r
+  // uses column buffer / exchange slot g * xrounds + r.
+  int xgpus, xrank, xblock, xexch, xemul, xrounds;
   const double* xin_abuf;             // rounds x cols x NP
   const unsigned long long* xin_prog;  // rounds x kXProg
   double* xout_abuf;
@@ -461,8 +464,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const int rb = min(32 * R, rows - row0);
   // strips: one column buffer per block round; pairs: slot of the pair
   const unsigned blk = b / static_cast<unsigned>(P.xblock);
-  const unsigned slot = P.xgpus > 1 || P.xexch ? blk / static_cast<unsigned>(P.xgpus)
-                                               : p % static_cast<unsigned>(P.slots);
+  const unsigned G = static_cast<unsigned>(P.xgpus);
+  // slot of block k's round on its GPU (xemul: per virtual GPU)
+  auto round_slot = [&](unsigned k) { return P.xemul ? (k % G) * static_cast<unsigned>(P.xrounds) + k / G : k / G; };
+  const unsigned slot = P.xgpus > 1 || P.xexch ? round_slot(blk) : p % static_cast<unsigned>(P.slots);
   const unsigned long long base = static_cast<unsigned long long>(p) * static_cast<unsigned long long>(cols + 1);
   double* colbuf = P.abuf + static_cast<size_t>(slot) * static_cast<size_t>(cols) * NP;
   unsigned long long* prog_row = P.prog + static_cast<size_t>(slot) * P.bands;
@@ -473,8 +478,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const bool xin = P.xexch && has_below && b % static_cast<unsigned>(P.xblock) == 0;
   const bool xout = P.xexch && has_above && (b + 1) % static_cast<unsigned>(P.xblock) == 0;
   const size_t xstride = static_cast<size_t>(cols) * NP;
-  const unsigned rin = blk / static_cast<unsigned>(P.xgpus);
-  const unsigned rout = (blk + 1) / static_cast<unsigned>(P.xgpus);
+  const unsigned rin = round_slot(blk);
+  const unsigned rout = round_slot(blk + 1);
   const double* in_buf = xin ? P.xin_abuf + rin * xstride : colbuf;
   const unsigned long long* in_prog = xin ? P.xin_prog + rin * kXProg : prog_row + (has_below ? b - 1 : 0);
   double* out_buf = xout ? P.xout_abuf + rout * xstride : colbuf;
@@ -1211,7 +1216,7 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 || LIT ? 1 : 
       p = g0 + (rem - bi * gcount);
       // strips: bi-th band of the blocks xrank, xrank + xgpus, ...
       const unsigned S = static_cast<unsigned>(P.xblock);
-      b = (static_cast<unsigned>(P.xrank) + static_cast<unsigned>(P.xgpus) * (bi / S)) * S + bi % S;
+      b = P.xemul ? bi : (static_cast<unsigned>(P.xrank) + static_cast<unsigned>(P.xgpus) * (bi / S)) * S + bi % S;
     } else {
       // segment DAG: claim the next cell of the ready list, wait for its unit
       unsigned u = 0;

@@ -248,17 +248,19 @@ def propagate_long_pair_distributed(x, y, order: int, options: Optional[sk.Propa
     return final, dg
 
 
-def propagate_split_emulated(x, y, order: int, block: int, options: Optional[sk.PropagateOptions] = None):
-    """One-GPU test of the strip protocol: a single launch whose hand-off
-    every `block` bands goes through an exchange area exactly as between
-    GPUs (sk_propagate_split)."""
+def propagate_split_emulated(x, y, order: int, block: int, options: Optional[sk.PropagateOptions] = None,
+                             gpus: int = 1):
+    """One-GPU test of the strip protocol: a single launch over all bands of
+    `gpus` virtual GPUs in the block-cyclic layout, every `block` bands handed
+    over through an exchange area exactly as between GPUs
+    (sk_propagate_split)."""
     x, y = sk._as_series(x), sk._as_series(y)
     lib = _capi.load()
     st = _capi.SkStatus()
     value = ctypes.c_double()
     xv, yv = x.values(), y.values()
     rc = lib.sk_propagate_split(sk._ptr(xv), x.length(), sk._ptr(yv), y.length(), x.dim(), int(order),
-                                sk._flags(options), int(block), ctypes.byref(value), ctypes.byref(st))
+                                sk._flags(options), int(gpus), int(block), ctypes.byref(value), ctypes.byref(st))
     sk._check(rc, st)
     return value.value
 

@@ -469,9 +469,11 @@ def test_gram_shards_reassemble(sk, restatement):
 
 # ------------------------------------------------------- multi-GPU strips
 def test_strip_protocol_emulated_on_one_gpu(sk, restatement):
-    """The long-pair strip hand-off (system-scope release/acquire through the
-    exchange areas, every `block` bands -- block = 1: at every band boundary)
-    inside one launch: bit-identical to the plain sweep, knots included."""
+    """The long-pair strip pipeline of 1, 2 and 3 virtual GPUs emulated in one
+    launch (block-cyclic column buffers and exchange areas per virtual GPU, the
+    hand-off every `block` bands -- block = 1: at every band boundary -- with
+    system-scope release/acquire, the last GPU handing to the first):
+    bit-identical to the plain sweep."""
     from paper_2502_20392_b200.distributed import propagate_split_emulated, strip_bands
     for d in (4, 12, 40):  # register kernel with shared-memory / direct top-row hand-up, large-d path
         x = restatement.brownian(300, d, 5)
@@ -481,7 +483,10 @@ def test_strip_protocol_emulated_on_one_gpu(sk, restatement):
             nb = strip_bands(400, order)
             assert nb >= 3
             for block in range(1, nb):
-                assert propagate_split_emulated(x, y, order, block) == plain, (d, order, block)
+                for gpus in (1, 2, 3):
+                    if -(-nb // block) < gpus:
+                        continue
+                    assert propagate_split_emulated(x, y, order, block, gpus=gpus) == plain, (d, order, block, gpus)
 
 
 def test_gram_over_a_device_list_matches_one_call(sk, restatement):
