@@ -561,6 +561,8 @@ def main():
         line["parity"]["in_run_pairs_checked"] = len(ref_vals)
         line["parity"]["in_run_max_rel_err"] = max(abs(A[i, j] - v) / abs(v) for (i, j), v in ref_vals.items())
     if rank == 0 and ws == 1 and not args.no_extras:
+        # the configs run on the library's own stream, not torch's default stream
+        lib.sk_set_stream(None, ctypes.byref(st))
         line["configs"] = extra_configs(sk, lib, st, _capi)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -502,7 +502,7 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
   int seg_cols = 0;
   unsigned spb = 0, units_pair = 0;
   if (bands > 1 && whole && std::getenv("SK_STREAM") == nullptr) {
-    const double warps_est = static_cast<double>(bps) * c.sms * kSweepWarps;
+    const double warps_est = static_cast<double>(bps) * c.sms * band_workers(ntempl, dp);
     const double pairs_launch = static_cast<double>(std::min(chunk, npairs_all));
     const double active = std::min(pairs_launch, 2.0 * warps_est);
     const double work_steps = pairs_launch * bands * (cols + 31.0) / warps_est;
