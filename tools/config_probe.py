@@ -2,7 +2,7 @@
 with sweep-kernel device time from the library's CUDA-event accounting.
 
   cfg1  single pair  l=1000,  d=2   adaptive
-  cfg3  single pair  l=L,     d=4   (default L = 1_000_001), sigma-scaled Brownian
+  cfg3  single pair  l=L,     d=4   (default L = 1_000_000), sigma-scaled Brownian
   cfg4  single pair  l=16384, d=512 (table path)
   cfg5  Gram m x m,  l=4096,  d=16  adaptive (default m = 128: a sample of the 1024 Gram)
 """
@@ -18,11 +18,9 @@ from paper_2502_20392_b200 import sigker as sk  # noqa: E402
 
 
 def brownian(n, length, dim, seed, sigma=1.0):
-    rng = np.random.default_rng(seed)
-    steps = rng.standard_normal((n, length - 1, dim)) * np.sqrt(1.0 / (length - 1)) * sigma
-    out = np.zeros((n, length, dim))
-    np.cumsum(steps, axis=1, out=out[:, 1:, :])
-    return out
+    """n series datagen::brownian(length, dim, seed + k) -- the reference's
+    generator, bit for bit (SURVEY.md section 8d inputs), times sigma."""
+    return sigma * sk.brownian_family(length, dim, [seed + k for k in range(n)])
 
 
 def timed(fn):
@@ -47,7 +45,7 @@ def report(name, tiles, wall, s, extra=""):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["cfg1", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--len3", type=int, default=1_000_001)
+    ap.add_argument("--len3", type=int, default=1_000_000)
     ap.add_argument("--sigma3", type=float, default=1.0)
     ap.add_argument("--m5", type=int, default=128)
     ap.add_argument("--warm", action="store_true", help="cfg5: one small Gram first (kernel loading, allocations)")
@@ -55,7 +53,7 @@ def main():
     pol = sk.TruncationPolicy.adaptive(1e-12)
     for cfg in a.configs:
         if cfg == "cfg1":
-            x, y = brownian(1, 1000, 2, 1)[0], brownian(1, 1000, 2, 2)[0]
+            x, y = brownian(1, 1000, 2, 1)[0], brownian(1, 1000, 2, 2)[0]  # seeds 1 / 2
             sk.propagate_with_policy(x, y, pol)
             r, wall, s = timed(lambda: sk.propagate_with_policy(x, y, pol))
             report("cfg1 l=1000 d=2", 999 * 999, wall, s, f"K={r.value!r} N={r.order}")
@@ -69,10 +67,10 @@ def main():
             x, y = brownian(1, 16384, 512, 1)[0], brownian(1, 16384, 512, 2)[0]
             sk.propagate_with_policy(x, y, pol, sk.PropagateOptions(strict_corner=False))
             r, wall, s = timed(lambda: sk.propagate_with_policy(x, y, pol, sk.PropagateOptions(strict_corner=False)))
-            report("cfg4 l=16384 d=512", 16383 ** 2, wall, s, f"K={r.value!r} N={r.order} (rho fused in the sweep)")
+            report("cfg4 l=16384 d=512", 16383 ** 2, wall, s, f"K={r.value!r} N={r.order} (large-d path: table mode where it fits, see DESIGN 4.3)")
         elif cfg == "cfg5":
             m = a.m5
-            fam = list(brownian(m, 4096, 16, 1000))
+            fam = brownian(m, 4096, 16, 1000)  # (m, l, d): gram_matrix's no-copy path
             if a.warm:
                 sk.gram_matrix(fam[:8], sk.GramOptions(policy=pol))
             r, wall, s = timed(lambda: sk.gram_matrix(fam, sk.GramOptions(policy=pol)))
