@@ -359,6 +359,19 @@ __device__ __forceinline__ bool wait_progress(const SweepParams& P, const unsign
 #endif
 }
 
+// one look at a progress counter, no waiting; warp-uniform: true only when
+// every lane's own acquire saw the count (each lane then reads what it covers)
+__device__ __forceinline__ bool poll_progress(const unsigned long long* ptr, unsigned long long need,
+                                              unsigned long long& seen, bool sys = false) {
+  bool ok = seen >= need;
+  if (!__all_sync(0xffffffffu, ok)) {
+    const unsigned long long v = sys ? ld_acquire_sys(ptr) : ld_acquire_gpu(ptr);
+    if (v >= need) seen = v;
+    ok = __all_sync(0xffffffffu, v >= need);
+  }
+  return ok;
+}
+
 // ---- ready list (segment-DAG mode, lane 0 only) ------------------------------
 // Every unit is pushed exactly once (the initial ones by the host), so the
 // list has units_total cells and never wraps: push takes the next cell with
@@ -849,13 +862,24 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     }
   };
 
+  // prefetch depth is one group, but only when its columns are already
+  // published: a caught-up band (latency-bound chains) stages the group it
+  // is about to run instead of waiting one group longer for the next one,
+  // which would add a whole group to every band's hand-over lag
+  int staged = c_begin;
   for (int c0 = c_begin * K, chunk = c_begin; c0 < steps && chunk < c_end; c0 += K, ++chunk) {
     __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
-    if (chunk + 1 < ngroups && chunk + 1 < c_end) {
+    if (staged < chunk && chunk < ngroups && chunk < c_end) {
       if (streaming && has_below &&
-          !wait_progress(P, in_prog, base + min(cols, (chunk + 2) * K), seen, p, b, xin))
+          !wait_progress(P, in_prog, base + min(cols, (chunk + 1) * K), seen, p, b, xin))
         return kBandAbort;
+      stage_group(chunk);
+      staged = chunk;
+    }
+    if (chunk + 1 < ngroups && chunk + 1 < c_end &&
+        (!(streaming && has_below) || poll_progress(in_prog, base + min(cols, (chunk + 2) * K), seen, xin))) {
       stage_group(chunk + 1);
+      staged = chunk + 1;
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
