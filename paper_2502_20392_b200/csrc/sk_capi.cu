@@ -650,8 +650,12 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.watchdog = c.wd.as<unsigned long long>();
     P.watchdog_ns = watchdog_ns();
     // with fewer pairs than warps, ~warps/group bands of each pair run at
-    // once; their natural spacing is one band time / (warps / group)
-    P.start_lag = group < warps ? static_cast<int>(0.75 * (cols + 32.0) * group / warps) : 0;
+    // once; when that is fewer than the pair's bands, a warp sweeps several
+    // of them in turn and their natural spacing is one band time / (warps /
+    // group).  With a warp per band the chain's hand-over is the only lag.
+    P.start_lag = group < warps && warps < group * static_cast<size_t>(bands)
+                      ? static_cast<int>(0.75 * (cols + 32.0) * group / warps)
+                      : 0;
     P.dot_err = dot_err;
     if (const char* e = std::getenv("SK_START_LAG")) P.start_lag = std::atoi(e);
     P.values = o.d_values;

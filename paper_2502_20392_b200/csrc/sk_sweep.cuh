@@ -304,6 +304,9 @@ __device__ unsigned long long g_wwait[1u << 14];
 __device__ unsigned g_tidx;
 #endif
 
+#ifndef SK_POLL_CAP
+#define SK_POLL_CAP 256  // ns: longest back-off between two polls of a progress counter
+#endif
 static __device__ __noinline__ bool wait_progress_slow(const unsigned long long* ptr, unsigned long long need,
                                                        unsigned long long& seen, unsigned long long* wd,
                                                        unsigned long long limit_ns, unsigned p, unsigned b,
@@ -314,7 +317,7 @@ static __device__ __noinline__ bool wait_progress_slow(const unsigned long long*
   unsigned ns = 32;
   for (unsigned it = 1;; ++it) {
     __nanosleep(ns);
-    if (ns < 1024) ns += ns >> 1;
+    if (ns < SK_POLL_CAP) ns += ns >> 1;
     if ((sys ? ld_relaxed_sys(ptr) : ld_relaxed_gpu(ptr)) >= need) break;
     if ((it & 15) == 0) {
       if (*reinterpret_cast<volatile unsigned long long*>(wd) != 0) return false;
