@@ -658,6 +658,10 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
                       : 0;
     P.dot_err = dot_err;
     if (const char* e = std::getenv("SK_START_LAG")) P.start_lag = std::atoi(e);
+    // large d, table mode, one pair at a time, streaming, one GPU's whole
+    // pair: consecutive bands share a CTA and hand alpha over in shared memory
+    P.intra = dp == 0 && use_table && ntempl > 0 && seg_here == 0 && group == 1 && whole &&
+              std::getenv("SK_NO_INTRA") == nullptr;
     P.values = o.d_values;
     P.err = o.d_err;
     P.maxrho = o.d_maxrho;

@@ -97,6 +97,12 @@ struct SweepParams {
   unsigned long long* watchdog;   // [0] abort flag, [1..4] first stuck wait (p, b, need, seen)
   unsigned long long watchdog_ns; // give up a dependency wait after this long
   int start_lag;                  // columns the band below must be ahead before a band starts
+  // DP == 0 table mode, one pair per launch group, streaming: each CTA claims
+  // rho_bands(N) consecutive bands per round, and a band whose neighbour
+  // below is the previous warp of the same CTA takes its alpha from that
+  // warp's shared-memory ring (CTA-scope counters) instead of the column
+  // buffer in global memory (release to L2, poll, staging copy)
+  int intra;
   double dot_err;                 // EXACT, N > 0: bound on |fused dot - sequential dot| for any tile
   double* values;                 // per output slot: K(1,1)
   unsigned long long* err;        // per output slot: min error key (init ~0)
@@ -272,7 +278,12 @@ struct RhoCtl {
   unsigned abort;       // the consumer abandoned the unit (watchdog)
   unsigned prod;        // blocks < prod are in the ring (absolute block index)
   unsigned cons;        // chunks < cons are done (absolute chunk index)
+  unsigned up_prod;     // intra: steps whose top-row alpha' is in this band's ring
+  unsigned up_cons;     // intra: steps of this band's ring the band above has copied
 };
+// intra hand-over ring: the top row's alpha' of the last kUpChunks chunks
+constexpr int kUpChunks = 8;
+constexpr unsigned kIntraBar = 15;  // named barrier of the CTA's sweep warps (intra rounds)
 
 __device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
   unsigned v;
@@ -474,6 +485,13 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const bool tab_mode = DP == 0 && P.rho_tab != nullptr;
   double* s_tab = smem + stage_doubles_per_warp(N, 0);
   const double* tab = DP > 0 || !tab_mode ? nullptr : P.rho_tab + static_cast<size_t>(p) * P.tab_stride;
+  // intra-CTA hand-over (SweepParams::intra): this band's ring after the
+  // staged table deltas; the band below is the previous warp's slot
+  constexpr int kUpRing = kUpChunks * K;  // steps held (power of two)
+  static_assert((kUpRing & (kUpRing - 1)) == 0, "intra ring index by mask");
+  double* const up_ring = smem + stage_doubles_per_warp(N, 0) + 2 * K * 32;
+  static_assert(DP > 0 || N == 0 || 2 * K * 32 + kUpRing * NP <= rho_ring_doubles() + rho_stage_doubles(),
+                "intra ring fits the slot's producer memory (unused in table mode)");
   const int n = N > 0 ? N + 1 : P.order + 1;
   const int rows = P.rows, cols = P.cols;
   const int row0 = static_cast<int>(b) * 32 * R;
@@ -489,6 +507,44 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   unsigned long long* prog_row = P.prog + static_cast<size_t>(slot) * P.bands;
   const bool has_below = b > 0;
   const bool has_above = b + 1 < static_cast<unsigned>(P.bands);
+  // (the kernel's slot of this warp: warp mod rho_bands)
+  const int kslot = DP == 0 ? static_cast<int>(threadIdx.x >> 5) % rho_bands(N) : 0;
+  const bool intra_in = DP == 0 && N > 0 && P.intra && has_below && kslot > 0;
+  const bool intra_out = DP == 0 && N > 0 && P.intra && has_above && kslot + 1 < rho_bands(N);
+  RhoCtl* const below_ctl = ctl - (intra_in ? 1 : 0);
+  const double* const below_ring = up_ring - (intra_in ? rho_slot_doubles(N) : 0);
+  // a dependency on the band below through global memory
+  const bool gdep = P.seg_cols == 0 && has_below && !intra_in;
+  // intra hand-over wait on a CTA-scope counter (lane 0 polls, the warp
+  // follows; gives up when the launch aborts or after the watchdog time)
+  auto intra_wait = [&](const unsigned* ctr, unsigned need) -> bool {
+    int stuck = 0;
+    if (lane == 0 && ld_acquire_cta_u32(ctr) < need) {
+      const unsigned long long t0 = globaltimer_ns();
+      unsigned ns = 16;
+      while (ld_acquire_cta_u32(ctr) < need) {
+        __nanosleep(ns);
+        if (ns < 128) ns *= 2;
+        if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) {
+          stuck = 1;
+          break;
+        }
+        if (globaltimer_ns() - t0 > P.watchdog_ns) {
+          if (atomicCAS(P.watchdog, 0ull, 1ull) == 0ull) {
+            P.watchdog[1] = p;
+            P.watchdog[2] = b;
+            P.watchdog[3] = need;
+            P.watchdog[4] = *reinterpret_cast<const volatile unsigned*>(ctr);
+          }
+          stuck = 1;
+          break;
+        }
+      }
+    }
+    const bool ok = __shfl_sync(0xffffffffu, stuck, 0) == 0;
+    __syncwarp();  // lane 0's acquire before every lane reads what it covers
+    return ok;
+  };
   // where this band's alpha comes from / goes to: the pair's column buffer,
   // or a cross-strip exchange buffer (multi-GPU long pair)
   const bool xin = P.xexch && has_below && b % static_cast<unsigned>(P.xblock) == 0;
@@ -588,7 +644,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   auto stage_group = [&](int g) {
     const int col0 = g * K;
     const int ncol = max(0, min(K, cols - col0));
-    if (has_below) {
+    if (has_below && !intra_in) {
       const double* src = in_buf + static_cast<size_t>(col0) * NP;
       double* dst = s_alpha + (g & 1) * kStage;
       const int pieces = ncol * NP / 2;
@@ -654,7 +710,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // start no closer than start_lag columns behind the band below: bands of
   // one pair then run evenly spread in time instead of bunched at the
   // minimum hand-over distance, where every timing jitter becomes a wait
-  if (streaming && has_below && !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin))
+  if (gdep && !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin))
     return kBandAbort;
   stage_group(c_begin);
 
@@ -835,7 +891,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   auto hand_up = [&](int c0, int kend) {
     // hand the top row's alpha' of this chunk to the band above, then publish
     // progress every kPublish columns
-    if (has_above) {
+    if (intra_out) {
+      __syncwarp();  // lane 31's ring writes before lane 0's release
+      if (lane == 0) st_release_cta_u32(&ctl->up_prod, static_cast<unsigned>(c0 + kend));
+    } else if (has_above) {
       const int jfirst = c0 - 31 - 32 * (R - 1);
       const int pieces = direct_top_out(DP) ? 0 : kend * NP / 2;
       for (int e = lane; e < pieces; e += 32) {
@@ -873,14 +932,12 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   for (int c0 = c_begin * K, chunk = c_begin; c0 < steps && chunk < c_end; c0 += K, ++chunk) {
     __syncwarp();  // everyone is done with the buffers group chunk + 1 overwrites
     if (staged < chunk && chunk < ngroups && chunk < c_end) {
-      if (streaming && has_below &&
-          !wait_progress(P, in_prog, base + min(cols, (chunk + 1) * K), seen, p, b, xin))
-        return kBandAbort;
+      if (gdep && !wait_progress(P, in_prog, base + min(cols, (chunk + 1) * K), seen, p, b, xin)) return kBandAbort;
       stage_group(chunk);
       staged = chunk;
     }
     if (chunk + 1 < ngroups && chunk + 1 < c_end &&
-        (!(streaming && has_below) || poll_progress(in_prog, base + min(cols, (chunk + 2) * K), seen, xin))) {
+        (!gdep || poll_progress(in_prog, base + min(cols, (chunk + 2) * K), seen, xin))) {
       stage_group(chunk + 1);
       staged = chunk + 1;
       cp_async_wait<1>();
@@ -888,6 +945,29 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       cp_async_wait<0>();
     }
     __syncwarp();
+    if (intra_in && c0 < cols) {
+      // columns [c0, c0 + K) of the band below: its top row's steps c0 + 31 ...
+      const int cend = min(cols, c0 + K);
+      const unsigned need = static_cast<unsigned>(cend + 31);
+      if (!intra_wait(&below_ctl->up_prod, need)) return kBandAbort;
+      double* dst = s_alpha + (chunk & 1) * kStage;
+      const int pieces = (cend - c0) * NP / 2;
+      for (int e = lane; e < pieces; e += 32) {
+        const int kk = e / (NP / 2);
+        const double* src = below_ring + ((c0 + kk + 31) & (kUpRing - 1)) * NP + (2 * e - kk * NP);
+        *reinterpret_cast<double2*>(dst + 2 * e) = *reinterpret_cast<const double2*>(src);
+      }
+      __syncwarp();  // every lane's ring reads before lane 0 frees the steps
+      if (lane == 0) st_release_cta_u32(&below_ctl->up_cons, need);
+      __syncwarp();
+    }
+    if (intra_out) {
+      // this chunk's top-row outputs go to ring chunk (chunk mod kUpChunks):
+      // the band above must have copied the steps it held
+      const int need = (chunk - kUpChunks + 1) * K;
+      if (need > 0 && !intra_wait(&ctl->up_cons, static_cast<unsigned>(need))) return kBandAbort;
+      s_out = up_ring + (chunk & (kUpChunks - 1)) * kStage;
+    }
     const double* stage = s_alpha + (chunk & 1) * kStage;
     const double* dl = DP > 0 ? s_delta : s_tab + (chunk & 1) * K * 32;
     const int kend = min(K, steps - c0);
@@ -1180,6 +1260,7 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 || LIT ? 1 : 
   static_assert(DP > 0 || kBands >= 1, "a band's shared memory must fit the SM");
   extern __shared__ __align__(16) double s_dyn[];
   __shared__ RhoCtl s_ctls[kBands];
+  __shared__ unsigned s_claim;  // intra: the CTA's first unit of this round
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int kslot = DP == 0 ? warp % kBands : 0;
@@ -1231,10 +1312,31 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 || LIT ? 1 : 
     if (P.seg_cols == 0) {
       // streaming: static unit order (group g, band b, pair q within the group)
       unsigned u = 0;
-      if (lane == 0) u = atomicAdd(P.queue, 1u);
-      u = __shfl_sync(0xffffffffu, u, 0);
-      if (u >= static_cast<unsigned>(P.npairs) * nb) break;
-      if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) break;
+      const unsigned total = static_cast<unsigned>(P.npairs) * nb;
+      if (DP == 0 && N > 0 && P.intra) {
+        // one round per CTA: its sweep warps meet, warp 0 claims kBands
+        // consecutive units (consecutive bands of one pair), warp w takes the
+        // w-th; the decision to stop is the same for every warp
+        named_bar_sync(kIntraBar, kBands * 32);
+        if (warp == 0 && lane == 0)
+          s_claim = *reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0
+                        ? ~0u
+                        : atomicAdd(P.queue, static_cast<unsigned>(kBands));
+        if (lane == 0) {
+          s_ctl.up_prod = 0u;
+          s_ctl.up_cons = 0u;
+        }
+        named_bar_sync(kIntraBar, kBands * 32);
+        const unsigned c0 = *reinterpret_cast<volatile unsigned*>(&s_claim);
+        if (c0 == ~0u || c0 >= total) break;
+        u = c0 + static_cast<unsigned>(kslot);
+        if (u >= total) continue;  // no unit this round; the next claim ends the loop
+      } else {
+        if (lane == 0) u = atomicAdd(P.queue, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= total) break;
+        if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0) break;
+      }
       const unsigned g = u / gsz;
       const unsigned rem = u - g * gsz;
       const unsigned g0 = g * static_cast<unsigned>(P.group);
@@ -1316,7 +1418,10 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 || LIT ? 1 : 
 #else
     const int st = run_unit(p, b, c_begin, c_end, restore, save);
 #endif
-    if (st == kBandAbort) break;
+    if (st == kBandAbort) {
+      if (DP == 0 && N > 0 && P.intra && P.seg_cols == 0) continue;  // the siblings meet at the next round (watchdog set)
+      break;
+    }
     if (P.seg_cols > 0) {
       __syncwarp();  // every lane's outputs before lane 0 releases them
       if (lane == 0) {
