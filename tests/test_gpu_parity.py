@@ -610,7 +610,9 @@ def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
     budget) and the fused producer warps (rho formed in shared memory, O(l)
     memory) run the same DMMA k-order or the same sequential dot, so every
     output is bit-identical -- values, orders, max|rho|, knot grids, literal
-    orders, error tiles, strict-corner decisions; both against the oracle."""
+    orders, error tiles, strict-corner decisions; both against the oracle.
+    The table mode's intra-CTA hand-over (consecutive bands of a single pair
+    in one CTA, alpha through shared memory) matches the global one too."""
     rng = restatement.rng(4242)
 
     def bits(v):
@@ -636,9 +638,13 @@ def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
         return out
 
     monkeypatch.setenv("SK_RHO_FUSED", "0")
-    table = run_all()
+    table = run_all()  # single pairs: consecutive bands hand over inside a CTA
+    monkeypatch.setenv("SK_NO_INTRA", "1")
+    table_global = run_all()  # every hand-over through the global column buffer
+    monkeypatch.delenv("SK_NO_INTRA")
     monkeypatch.setenv("SK_RHO_FUSED", "1")
     fused = run_all()
+    assert table_global == table
     assert fused == table
     v_ref, _ = restatement.propagate(x1, y1, 20)
     assert sk.propagate(x1, y1, 20).value == v_ref
