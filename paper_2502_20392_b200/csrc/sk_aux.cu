@@ -186,18 +186,31 @@ __global__ void rho_table_exact_kernel(const double* __restrict__ xinc, const do
 // rho = dY * dX^T.  CTA tile 64 x 64 (i x j), 4 warps of 32 x 32, k staged
 // through shared memory in chunks of 32 with cp.async double buffering.
 // Increments are zero-padded to ld (multiple of 4), so k-padding is exact.
+// GK = k chunk: 32 alone (74 KB of shared memory, 3 CTAs per SM), 16 when the
+// GEMM runs beside a latency-bound sweep (41 KB: two fit next to a sweep CTA).
+// rowdone (optional): per pair and 64-row block, the number of column blocks
+// written -- the sweep's bands start on their rows as soon as they are done.
 constexpr int kGT = 64;            // CTA tile edge
-constexpr int kGK = 32;            // k chunk
-constexpr int kGS = kGK + 4;       // smem row stride (doubles): conflict-free fragment loads
-constexpr int kGemmSmem = 2 * 2 * kGT * kGS * 8;
+template <int GK>
+constexpr int gemm_smem() {
+  return 2 * 2 * kGT * (GK + 4) * 8;  // [buf][A|B][kGT][GK + 4]: conflict-free fragment loads
+}
 
+#ifndef SK_OVERLAP_GK
+#define SK_OVERLAP_GK 16
+#endif
+constexpr int kOverlapGK = SK_OVERLAP_GK;
 
+template <int GK>
 __global__ void __launch_bounds__(128) rho_gemm_kernel(const double* __restrict__ xinc,
                                                        const double* __restrict__ yinc,
                                                        const uint32_t* __restrict__ px,
                                                        const uint32_t* __restrict__ py, unsigned long long sx,
                                                        unsigned long long sy, int rows, int cols, int ld,
-                                                       double* __restrict__ tab, unsigned long long tab_stride) {
+                                                       double* __restrict__ tab, unsigned long long tab_stride,
+                                                       unsigned* __restrict__ rowdone) {
+  constexpr int kGK = GK;
+  constexpr int kGS = GK + 4;
   extern __shared__ __align__(16) double gsm[];  // [buf][A|B][kGT][kGS]
   const int pr = blockIdx.z;
   const int i0 = blockIdx.y * kGT, j0 = blockIdx.x * kGT;
@@ -263,6 +276,14 @@ __global__ void __launch_bounds__(128) rho_gemm_kernel(const double* __restrict_
       const int j = j0 + wn * 32 + nt * 8 + 2 * (lane & 3);
       if (j < cols) out[static_cast<size_t>(i) * cols + j] = acc[mt][nt][0];
       if (j + 1 < cols) out[static_cast<size_t>(i) * cols + j + 1] = acc[mt][nt][1];
+    }
+  }
+  if (rowdone != nullptr) {
+    // every thread's tile stores, then one gpu-scope fence and count
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(rowdone + static_cast<size_t>(pr) * gridDim.y + blockIdx.y, 1u);
     }
   }
 }
@@ -417,7 +438,7 @@ cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uin
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
                              int dim, int ld, bool exact, double* tab, unsigned long long tab_stride,
-                             cudaStream_t st) {
+                             cudaStream_t st, unsigned* rowdone) {
   if (npairs == 0) return cudaSuccess;
   if (exact) {
     const dim3 grid((cols + 31) / 32, (rows + 7) / 8, static_cast<unsigned>(npairs));
@@ -432,12 +453,20 @@ cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint3
   if (e != cudaSuccess) return e;
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-    e = cudaFuncSetAttribute(rho_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    e = cudaFuncSetAttribute(rho_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem<32>());
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(rho_gemm_kernel<kOverlapGK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             gemm_smem<kOverlapGK>());
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   const dim3 grid((cols + kGT - 1) / kGT, (rows + kGT - 1) / kGT, static_cast<unsigned>(npairs));
-  rho_gemm_kernel<<<grid, 128, kGemmSmem, st>>>(xinc, yinc, px, py, sx, sy, rows, cols, ld, tab, tab_stride);
+  if (rowdone != nullptr)
+    rho_gemm_kernel<kOverlapGK><<<grid, 128, gemm_smem<kOverlapGK>(), st>>>(xinc, yinc, px, py, sx, sy, rows, cols,
+                                                                            ld, tab, tab_stride, rowdone);
+  else
+    rho_gemm_kernel<32><<<grid, 128, gemm_smem<32>(), st>>>(xinc, yinc, px, py, sx, sy, rows, cols, ld, tab,
+                                                            tab_stride, nullptr);
   return cudaGetLastError();
 }
 

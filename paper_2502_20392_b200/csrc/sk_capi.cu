@@ -192,8 +192,26 @@ struct Ctx {
   std::vector<void*> stage;
   std::vector<cudaEvent_t> stage_ev;
 
+  // cfg-4 overlap: the rho GEMM runs on `side` beside the sweep on stream()
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevBuf rowdone;  // per pair and 64-row block: GEMM tiles written
+
   cudaStream_t stream() const { return user ? user : own; }
+  int ensure_side() {
+    if (side) return 0;
+    int prio_lo = 0, prio_hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess) return 1;
+    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio_lo) != cudaSuccess) return 1;
+    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess) return 1;
+    if (cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) return 1;
+    return 0;
+  }
   ~Ctx() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+    rowdone.release();
     for (void* p : stage) cudaFreeHost(p);
     for (cudaEvent_t e : stage_ev) cudaEventDestroy(e);
     for (auto& r : stats) {
@@ -225,7 +243,12 @@ int get_ctx(Ctx** out, sk_status* st) {
     auto c = std::make_unique<Ctx>();
     c->device = t_device;
     SK_CUDA(cudaSetDevice(c->device));
-    SK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    // the library's stream at the highest priority: where a launch runs a
+    // helper kernel beside it (the cfg-4 GEMM on `side`), its CTAs are
+    // dispatched first
+    int prio_lo = 0, prio_hi = 0;
+    SK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SK_CUDA(cudaStreamCreateWithPriority(&c->own, cudaStreamNonBlocking, prio_hi));
     SK_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
     // W table, row stride 65 (tile_series.cpp:41-53 build_W_into)
     const double* fact = host_factorials();
@@ -614,13 +637,26 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
                               cudaMemcpyHostToDevice, c.stream()));
       SK_CUDA(cudaStreamSynchronize(c.stream()));  // `init` is pageable host memory
     }
+    // cfg 4 (one large-d pair at a time, latency-bound sweep): the DMMA GEMM
+    // runs beside the sweep on a second stream and publishes each 64-row
+    // block as it completes; the sweep (compact layout, no producer warps)
+    // leaves the SMs' tensor pipe, most issue slots and 110 KB of shared
+    // memory free for it
+    const bool overlap = use_table && ntempl > 0 && !lit && seg_here == 0 && group == 1 && whole &&
+                         std::getenv("SK_NO_OVERLAP") == nullptr && c.ensure_side() == 0;
+    const int nrb = (rows + 63) / 64, ncb = (cols + 63) / 64;
     if (use_table) {
       SK_CUDA(c.tab.ensure(npairs * tab_elems * sizeof(double)));
-      // exact (sequential) deltas for the literal kernel, DMMA otherwise (the
-      // EXACT max|rho| re-forms candidates with the sequential dot)
-      SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, ps.dim, ps.ld,
-                               ntempl == 0 || lit, c.tab.as<double>(), tab_elems, c.stream()));
-      ++c.aux_launches;
+      if (overlap) {
+        SK_CUDA(c.rowdone.ensure(npairs * nrb * sizeof(unsigned)));
+        SK_CUDA(cudaMemsetAsync(c.rowdone.p, 0, npairs * nrb * sizeof(unsigned), c.stream()));
+      } else {
+        // exact (sequential) deltas for the literal kernel, DMMA otherwise (the
+        // EXACT max|rho| re-forms candidates with the sequential dot)
+        SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, ps.dim, ps.ld,
+                                 ntempl == 0 || lit, c.tab.as<double>(), tab_elems, c.stream()));
+        ++c.aux_launches;
+      }
     }
     SweepParams P{};
     P.xinc = ps.d_xinc;
@@ -689,11 +725,32 @@ int run_sweeps(Ctx& c, const PairSet& ps, const std::vector<uint32_t>& px, const
     P.rq = seg_here ? c.rq.as<unsigned>() : nullptr;
     P.ctr = c.queue.as<unsigned>() + kCtrLine;
 
+    if (overlap) {
+      P.rho_ready = c.rowdone.as<unsigned>();
+      P.rho_ready_need = static_cast<unsigned>(ncb);
+      P.rho_ready_nrb = nrb;
+      P.slot_stride = table_slot_doubles(ntempl);
+    }
+
     StatRec rec{};
     rec.tiles = static_cast<double>(npairs) * rows * cols;
     rec.flops = rec.tiles * flops_per_tile(order, ps.dim);
     if (int rc = record_start(c, &rec, st)) return rc;
+    if (overlap) {
+      // the GEMM is queued FIRST: the sweep waits on it, never the reverse,
+      // so even streams that the driver serialises (one hardware queue)
+      // cannot deadlock -- they only lose the overlap
+      SK_CUDA(cudaEventRecord(c.ev_fork, c.stream()));
+      SK_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+      SK_CUDA(launch_rho_table(ps.d_xinc, ps.d_yinc, d_px, d_py, npairs, ps.sx, ps.sy, rows, cols, ps.dim, ps.ld,
+                               false, c.tab.as<double>(), tab_elems, c.side, c.rowdone.as<unsigned>()));
+      ++c.aux_launches;
+    }
     SK_CUDA(sweep_launch(ntempl, dp, exact, extras, lit, blocks, c.stream(), P));
+    if (overlap) {
+      SK_CUDA(cudaEventRecord(c.ev_join, c.side));
+      SK_CUDA(cudaStreamWaitEvent(c.stream(), c.ev_join, 0));
+    }
     if (int rc = record_end(c, &rec, st)) return rc;
     ++c.sweep_launches;
     if (int rc = check_watchdog(c, st)) return rc;

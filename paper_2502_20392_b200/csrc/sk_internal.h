@@ -40,10 +40,12 @@ cudaError_t launch_maxrho_scan(const double* xinc, const double* yinc, const uin
                                int dim, int ld, unsigned long long* out, cudaStream_t st);
 // rho[i][j] tables (rows x cols, row-major) for the large-d path when they
 // fit the memory budget: DMMA GEMM, or the bit-exact sequential dot when `exact`.
+// rowdone (DMMA only, optional): npairs x ceil(rows / 64) counters, each
+// counting the 64 x 64 tiles of its row block written (ceil(cols / 64) when done).
 cudaError_t launch_rho_table(const double* xinc, const double* yinc, const uint32_t* px, const uint32_t* py,
                              size_t npairs, unsigned long long sx, unsigned long long sy, int rows, int cols,
                              int dim, int ld, bool exact, double* tab, unsigned long long tab_stride,
-                             cudaStream_t st);
+                             cudaStream_t st, unsigned* rowdone = nullptr);
 cudaError_t launch_reset_slots(const uint32_t* idx, size_t n, unsigned long long* err, cudaStream_t st);
 cudaError_t launch_gather_slots(const uint32_t* idx, size_t n, const double* values, const unsigned long long* err,
                                 unsigned long long* out, cudaStream_t st);

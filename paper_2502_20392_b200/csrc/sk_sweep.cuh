@@ -103,6 +103,16 @@ struct SweepParams {
   // warp's shared-memory ring (CTA-scope counters) instead of the column
   // buffer in global memory (release to L2, poll, staging copy)
   int intra;
+  // table mode beside a running GEMM (cfg 4 overlap): the GEMM counts the
+  // 64 x 64 tiles written per 64-row block (rho_ready[pair * rho_ready_nrb +
+  // block], rho_ready_need when complete) and a band starts once its block is
+  // done.  slot_stride (doubles, > 0): the compact table-mode slot layout and
+  // rho_bands(N) sweep warps per CTA (no producer warps), so GEMM CTAs fit
+  // beside the sweep CTA.  Null / 0: the table is complete at launch.
+  const unsigned* rho_ready;
+  unsigned rho_ready_need;
+  int rho_ready_nrb;
+  int slot_stride;
   double dot_err;                 // EXACT, N > 0: bound on |fused dot - sequential dot| for any tile
   double* values;                 // per output slot: K(1,1)
   unsigned long long* err;        // per output slot: min error key (init ~0)
@@ -282,7 +292,19 @@ struct RhoCtl {
   unsigned up_cons;     // intra: steps of this band's ring the band above has copied
 };
 // intra hand-over ring: the top row's alpha' of the last kUpChunks chunks
-constexpr int kUpChunks = 8;
+constexpr int kUpChunks = 4;
+// shared memory a compact table-mode sweep CTA requests: > half the SM's
+// 228 KB, so two never share an SM, and leaves room for two 41 KB GEMM CTAs
+#ifndef SK_TABLE_CTA_KB
+#define SK_TABLE_CTA_KB 118
+#endif
+constexpr size_t kTableCtaSmem = SK_TABLE_CTA_KB * 1024;
+// compact table-mode slot (SweepParams::slot_stride): stage | staged table
+// deltas (2 x K x 32) | intra ring
+__host__ __device__ constexpr int table_slot_doubles(int N) {
+  return stage_doubles_per_warp(N, 0) + 2 * chunk_cols(rows_per_lane(N)) * 32 +
+         kUpChunks * chunk_cols(rows_per_lane(N)) * col_stride(N);
+}
 constexpr unsigned kIntraBar = 15;  // named barrier of the CTA's sweep warps (intra rounds)
 
 __device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
@@ -512,7 +534,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   const bool intra_in = DP == 0 && N > 0 && P.intra && has_below && kslot > 0;
   const bool intra_out = DP == 0 && N > 0 && P.intra && has_above && kslot + 1 < rho_bands(N);
   RhoCtl* const below_ctl = ctl - (intra_in ? 1 : 0);
-  const double* const below_ring = up_ring - (intra_in ? rho_slot_doubles(N) : 0);
+  const double* const below_ring =
+      up_ring - (intra_in ? (P.slot_stride > 0 ? P.slot_stride : rho_slot_doubles(N)) : 0);  // the kernel's slot stride
   // a dependency on the band below through global memory
   const bool gdep = P.seg_cols == 0 && has_below && !intra_in;
   // intra hand-over wait on a CTA-scope counter (lane 0 polls, the warp
@@ -543,6 +566,34 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     }
     const bool ok = __shfl_sync(0xffffffffu, stuck, 0) == 0;
     __syncwarp();  // lane 0's acquire before every lane reads what it covers
+    return ok;
+  };
+  // table beside a running GEMM: this band's 64-row block of the table
+  auto rows_ready = [&]() -> bool {
+    const unsigned* ctr = P.rho_ready + static_cast<size_t>(p) * P.rho_ready_nrb + row0 / 64;
+    const unsigned need = P.rho_ready_need;
+    int stuck = 0;
+    if (lane == 0 && ld_acquire_u32(ctr) < need) {
+      const unsigned long long t0 = globaltimer_ns();
+      unsigned ns = 64;
+      while (ld_acquire_u32(ctr) < need) {
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
+        if (*reinterpret_cast<volatile unsigned long long*>(P.watchdog) != 0 ||
+            globaltimer_ns() - t0 > P.watchdog_ns) {
+          if (atomicCAS(P.watchdog, 0ull, 1ull) == 0ull) {
+            P.watchdog[1] = p;
+            P.watchdog[2] = b;
+            P.watchdog[3] = need;
+            P.watchdog[4] = *reinterpret_cast<const volatile unsigned*>(ctr);
+          }
+          stuck = 1;
+          break;
+        }
+      }
+    }
+    const bool ok = __shfl_sync(0xffffffffu, stuck, 0) == 0;
+    __syncwarp();  // lane 0's acquire before every lane gathers table rows
     return ok;
   };
   // where this band's alpha comes from / goes to: the pair's column buffer,
@@ -712,6 +763,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   // minimum hand-over distance, where every timing jitter becomes a wait
   if (gdep && !wait_progress(P, in_prog, base + min(cols, max(K, P.start_lag)), seen, p, b, xin))
     return kBandAbort;
+  if (DP == 0 && tab_mode && P.rho_ready != nullptr && !rows_ready()) return kBandAbort;
   stage_group(c_begin);
 
   // one step = R tiles of this lane (one basic block, conditional work predicated)
@@ -1266,7 +1318,8 @@ __global__ void __launch_bounds__(sweep_warps(N, DP) * 32, DP == 0 || LIT ? 1 : 
   const int kslot = DP == 0 ? warp % kBands : 0;
   RhoCtl& s_ctl = s_ctls[kslot];
   const unsigned bar_start = 1u + 2u * kslot, bar_end = 2u + 2u * kslot;
-  double* smem = DP == 0 ? s_dyn + kslot * rho_slot_doubles(N) : s_dyn + warp * stage_doubles_per_warp(N, DP, LIT);
+  double* smem = DP == 0 ? s_dyn + kslot * (P.slot_stride > 0 ? P.slot_stride : rho_slot_doubles(N))
+                         : s_dyn + warp * stage_doubles_per_warp(N, DP, LIT);
   if constexpr (DP == 0) {
     if (warp >= kBands) {
       if (P.rho_tab != nullptr) return;  // table mode: no producers

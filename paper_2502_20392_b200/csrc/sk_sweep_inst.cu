@@ -2,6 +2,7 @@
 // (Makefile) so the 17 x 5 x 2 sweep instantiations build in parallel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -57,7 +58,17 @@ static cudaError_t launch_one(int grid, cudaStream_t stream, const SweepParams& 
     cudaMemsetAsync(tp, 0, kTraceUnits * 4 * sizeof(unsigned long long), stream);
   }
 #endif
-  sweep_kernel<N, DP, EXACT, EXTRAS, LIT><<<grid, sweep_warps(N, DP) * 32, smem_bytes<N, DP, EXACT, EXTRAS, LIT>(), stream>>>(P);
+  // compact table-mode layout (slot_stride): sweep warps only, the slots
+  // packed, and at least kTableCtaSmem requested so that two sweep CTAs never
+  // share an SM (one latency-bound sweep warp per sub-partition) while two
+  // GEMM CTAs still fit beside one
+  int threads = sweep_warps(N, DP) * 32;
+  size_t smem = smem_bytes<N, DP, EXACT, EXTRAS, LIT>();
+  if (DP == 0 && P.slot_stride > 0) {
+    threads = rho_bands(N) * 32;
+    smem = std::max(static_cast<size_t>(rho_bands(N)) * P.slot_stride * sizeof(double), kTableCtaSmem);
+  }
+  sweep_kernel<N, DP, EXACT, EXTRAS, LIT><<<grid, threads, smem, stream>>>(P);
 #ifdef SK_PROFILE_WAITS
   if (const char* path = std::getenv("SK_UTRACE")) {
     static std::vector<unsigned long long> h(kTraceUnits * 4);
