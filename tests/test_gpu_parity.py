@@ -612,7 +612,8 @@ def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
     output is bit-identical -- values, orders, max|rho|, knot grids, literal
     orders, error tiles, strict-corner decisions; both against the oracle.
     The table mode's intra-CTA hand-over (consecutive bands of a single pair
-    in one CTA, alpha through shared memory) matches the global one too."""
+    in one CTA, alpha through shared memory) and the GEMM running beside the
+    sweep match the serial, global-memory path too."""
     rng = restatement.rng(4242)
 
     def bits(v):
@@ -638,10 +639,14 @@ def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
         return out
 
     monkeypatch.setenv("SK_RHO_FUSED", "0")
-    table = run_all()  # single pairs: consecutive bands hand over inside a CTA
+    # single pairs: consecutive bands hand over inside a CTA, and the GEMM
+    # runs beside the sweep (bands start on published row blocks)
+    table = run_all()
     monkeypatch.setenv("SK_NO_INTRA", "1")
-    table_global = run_all()  # every hand-over through the global column buffer
+    monkeypatch.setenv("SK_NO_OVERLAP", "1")
+    table_global = run_all()  # every hand-over through global memory, GEMM first
     monkeypatch.delenv("SK_NO_INTRA")
+    monkeypatch.delenv("SK_NO_OVERLAP")
     monkeypatch.setenv("SK_RHO_FUSED", "1")
     fused = run_all()
     assert table_global == table
