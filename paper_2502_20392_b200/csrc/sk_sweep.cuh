@@ -217,8 +217,15 @@ __host__ __device__ constexpr bool direct_top_out(int DP) { return DP >= SK_DIRE
 // per chunk: the literal kernels (exact sequential dots); the register
 // kernels form each tile's product inside the step (d <= 16)
 __host__ __device__ constexpr bool chunk_deltas(int N, int DP, bool lit) { return DP > 0 && (N == 0 || lit); }
+// lane-to-lane alpha slot buffers: two (written at step s into buffer s mod 2,
+// read at step s + 1), so one warp barrier per step orders both the reads
+// before the rewrite and the writes before the reads
+#ifndef SK_PASS_BUFS
+#define SK_PASS_BUFS 2
+#endif
+constexpr int kPassBufs = SK_PASS_BUFS;
 __host__ __device__ constexpr int stage_doubles_per_warp(int N, int DP, bool lit = false) {
-  return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + 32 * rows_per_lane(N) * col_stride(N) +
+  return 2 * chunk_cols(rows_per_lane(N)) * col_stride(N) + kPassBufs * 32 * rows_per_lane(N) * col_stride(N) +
          (direct_top_out(DP) ? 0 : chunk_cols(rows_per_lane(N)) * col_stride(N)) +
          (DP > 0 ? ring_rows(rows_per_lane(N)) * ring_stride(DP) : 0) +
          (chunk_deltas(N, DP, lit) ? rows_per_lane(N) * chunk_cols(rows_per_lane(N)) * 32 : 0);
@@ -498,7 +505,11 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
   constexpr bool kLiteral = N == 0 || LIT;
   double* s_alpha = smem;                                   // 2 x K x NP
   double* s_pass = s_alpha + 2 * kStage;                    // 32 R x NP: slot (32 r + t) = row 32 r + t
-  double* s_out = s_pass + 32 * R * NP;                     // K x NP
+  double* s_out = s_pass + kPassBufs * 32 * R * NP;         // K x NP
+  constexpr int kPassBuf = 32 * R * NP;  // one slot buffer
+  // the slot buffer step s reads (written at step s - 1) / writes
+  auto pass_in = [&](int s) { return s_pass + (kPassBufs == 2 ? ((s - 1) & 1) * kPassBuf : 0); };
+  auto pass_out = [&](int s) { return s_pass + (kPassBufs == 2 ? (s & 1) * kPassBuf : 0); };
   double* s_ring = s_out + (direct_top_out(DP) ? 0 : kStage);  // RING x XS (DP > 0)
   double* s_delta = s_ring + (DP > 0 ? RING * XS : 0);      // [r][k][lane] (DP > 0)
   // DP == 0: the producers' rho ring, column c of row t at [(c mod kRhoW) * 32 + t];
@@ -736,9 +747,11 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
 #pragma unroll
       for (int m = 0; m < NA; ++m)
         if (NA <= kMaxRegOrder + 1 || m < n) roA[r][m] = rec[(r * NP + m) * 32 + lane];
-    for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = rec[32 * R * NP + e];
+    double* const sp0 = pass_in(c_begin * K);
+    for (int e = lane; e < 32 * R * NP; e += 32) sp0[e] = rec[32 * R * NP + e];
   } else {
-    for (int e = lane; e < 32 * R * NP; e += 32) s_pass[e] = (e % NP == 0) ? 1.0 : 0.0;
+    double* const sp0 = pass_in(c_begin * K);
+    for (int e = lane; e < 32 * R * NP; e += 32) sp0[e] = (e % NP == 0) ? 1.0 : 0.0;
   }
   if constexpr (DP > 0) {
     // dx of the columns the lanes still need behind the first staged group,
@@ -775,10 +788,10 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
     // lane 0's tile r >= 1 reads lane 31's tile r - 1
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double* src = (r == 0 && lane == 0) ? stage + k * NP : s_pass + (32 * r + lane - 1) * NP;
+      const double* src = (r == 0 && lane == 0) ? stage + k * NP : pass_in(s) + (32 * r + lane - 1) * NP;
       lds_series<NA>(src, q[r], n);
     }
-    __syncwarp();  // every slot has been read before any is rewritten
+    if constexpr (kPassBufs == 1) __syncwarp();  // every slot has been read before any is rewritten
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int j = s - lane - 32 * r;
@@ -822,7 +835,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       if constexpr (direct_top_out(DP)) {
         // every row in its slot (the top lane's slot is never read); the top
         // row's alpha' straight to the column buffer of the band above
-        sts_series<NA>(s_pass + (32 * r + lane) * NP, qo, n);
+        sts_series<NA>(pass_out(s) + (32 * r + lane) * NP, qo, n);
         if (r == R - 1) {
           const bool up = has_above && lane == 31 && j >= 0 && j < cols;
           double* dst = out_buf + static_cast<size_t>(up ? j : 0) * NP;
@@ -830,7 +843,7 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
           for (int m = 0; m < NA; m += 2) st_global_cg2_if(up, dst + m, qo[m], m + 1 < NA ? qo[m + 1] : 0.0);
         }
       } else {
-        sts_series<NA>((r == R - 1 && lane == 31) ? s_out + k * NP : s_pass + (32 * r + lane) * NP, qo, n);
+        sts_series<NA>((r == R - 1 && lane == 31) ? s_out + k * NP : pass_out(s) + (32 * r + lane) * NP, qo, n);
       }
 
       const bool active = row_ok[r] && j >= 0 && j < cols;
@@ -1131,7 +1144,9 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
 #pragma unroll
       for (int m = 0; m < NA; ++m)
         if (NA <= kMaxRegOrder + 1 || m < n) rec[(r * NP + m) * 32 + lane] = roA[r][m];
-    for (int e = lane; e < 32 * R * NP; e += 32) rec[32 * R * NP + e] = s_pass[e];
+    // the slots the unit's last step wrote (what the next step would read)
+    const double* const spl = pass_in(static_cast<int>(min(static_cast<long long>(c_end) * K, static_cast<long long>(steps))));
+    for (int e = lane; e < 32 * R * NP; e += 32) rec[32 * R * NP + e] = spl[e];
   }
   // per-pair error key (first failing tile) and max|delta|: min / max
   // reductions, so each segment flushes its part
