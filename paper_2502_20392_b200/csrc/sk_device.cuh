@@ -63,6 +63,13 @@ __device__ __forceinline__ bool corner_mismatch(double a0, double b0, double tol
   const double d = fabs(a0 - b0);
   return (d > tol) & (d > tol * fabs(a0)) & (d > tol * fabs(b0));
 }
+// The register kernels' screen in three FP64 operations: |a0 - b0| >
+// s (1 + |a0|) flags every tile the reference's test flags, because
+// max(1, |a0|, |b0|) >= (1 + |a0|) / 2 and s = 1e-11 sits 50x below 1e-9 / 2
+// (room for the register solver's different rounding of a0 and b0).
+__device__ __forceinline__ bool corner_screen(double a0, double b0) {
+  return fabs(a0 - b0) > fma(kCornerScreen, fabs(a0), kCornerScreen);
+}
 
 // Sequential non-FMA dot product in coordinate order: bit-identical to
 // `acc += a[c] * b[c]` at the reference's shipped flags

@@ -850,7 +850,8 @@ __device__ __forceinline__ int sweep_band(const SweepParams& P, unsigned p, unsi
       // the reference's throw order inside a tile: delta guard (checked when
       // the chunk's deltas are formed), corner check, non-finite total
       // (wavefront.cpp:150-173); the first failing tile of the row wins
-      const bool cm = strict & corner_mismatch(q[r][0], r_in[r][0], kLiteral ? kCornerTol : kCornerScreen);
+      const bool cm = strict & (kLiteral ? corner_mismatch(q[r][0], r_in[r][0], kCornerTol)
+                                         : corner_screen(q[r][0], r_in[r][0]));
       const bool nf = (TOT || kLiteral) && !isfinite(total);
       const unsigned code = cm ? kErrCorner : (nf ? kErrNonFinite : 0u);
       const unsigned kk = (static_cast<unsigned>(j) << 2) | code;
