@@ -656,6 +656,37 @@ def test_large_d_fused_rho_matches_table(sk, restatement, monkeypatch):
     assert rel(sk.propagate(x1, y1, 8).value, restatement.propagate(x1, y1, 8)[0]) < TOL
 
 
+def test_large_d_intra_and_overlap_across_pairs(sk, restatement, monkeypatch):
+    """d > 16, streaming, one pair per group but several pairs per launch
+    (SK_FORCE_GROUP=1): intra-CTA claims straddle the pairs' band ranges and
+    the GEMM beside the sweep publishes row blocks per pair.  Band counts not
+    multiples of four, tall and wide pairs; bit-identical to the serial,
+    global-memory path, and to the oracle within tolerance."""
+    rng = restatement.rng(777)
+    xs = np.stack([rng.random_series(97, 24, 1.0) for _ in range(3)])
+    ys = np.stack([rng.random_series(161, 24, 1.0) for _ in range(3)])
+
+    def bits(v):
+        return np.ascontiguousarray(v, dtype=np.float64).view(np.int64).tolist()
+
+    def run():
+        a = sk.pairwise(xs, ys, sk.TruncationPolicy.fixed(8), want_max_abs_rho=True)
+        b = sk.pairwise(ys, xs, sk.TruncationPolicy.fixed(8))
+        return bits(a.values), bits(a.max_abs_rho), bits(b.values)
+
+    monkeypatch.setenv("SK_RHO_FUSED", "0")
+    monkeypatch.setenv("SK_STREAM", "1")
+    monkeypatch.setenv("SK_FORCE_GROUP", "1")
+    fast = run()
+    monkeypatch.setenv("SK_NO_INTRA", "1")
+    monkeypatch.setenv("SK_NO_OVERLAP", "1")
+    serial = run()
+    assert fast == serial
+    for k in range(3):
+        ref, _ = restatement.propagate(xs[k], ys[k], 8)
+        assert rel(np.array(fast[0], dtype=np.int64).view(np.float64)[k], ref) < TOL
+
+
 @pytest.mark.parametrize("kernel", ["register", "runtime"])
 def test_literal_kernels_bit_identical_to_the_reference(sk, restatement, monkeypatch, kernel):
     """The literal kernels -- the order-8 register-resident one the strict
