@@ -199,12 +199,21 @@ struct Ctx {
 
   cudaStream_t stream() const { return user ? user : own; }
   int ensure_side() {
-    if (side) return 0;
+    if (side && ev_fork && ev_join) return 0;  // (a partial failure retries the missing pieces)
     int prio_lo = 0, prio_hi = 0;
     if (cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess) return 1;
-    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio_lo) != cudaSuccess) return 1;
-    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess) return 1;
-    if (cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) return 1;
+    if (!side && cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio_lo) != cudaSuccess) {
+      side = nullptr;
+      return 1;
+    }
+    if (!ev_fork && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+      ev_fork = nullptr;
+      return 1;
+    }
+    if (!ev_join && cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      ev_join = nullptr;
+      return 1;
+    }
     return 0;
   }
   ~Ctx() {
