@@ -204,14 +204,17 @@ struct Ctx {
     if (cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess) return 1;
     if (!side && cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio_lo) != cudaSuccess) {
       side = nullptr;
+      cudaGetLastError();  // the overlap is skipped; later launches must not see this error
       return 1;
     }
     if (!ev_fork && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess) {
       ev_fork = nullptr;
+      cudaGetLastError();  // the overlap is skipped; later launches must not see this error
       return 1;
     }
     if (!ev_join && cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess) {
       ev_join = nullptr;
+      cudaGetLastError();  // the overlap is skipped; later launches must not see this error
       return 1;
     }
     return 0;
