@@ -687,6 +687,27 @@ def test_large_d_intra_and_overlap_across_pairs(sk, restatement, monkeypatch):
         assert rel(np.array(fast[0], dtype=np.int64).view(np.float64)[k], ref) < TOL
 
 
+def test_large_d_fast_paths_randomised(sk, monkeypatch):
+    """Random large-d single pairs (d 17..130, lengths 40..900, orders 4/8/12):
+    the intra-CTA hand-over and the GEMM beside the sweep are bit-identical
+    to the serial global-memory path (tools/large_d_stress.py at scale)."""
+    rng = np.random.default_rng(5)
+    opts = sk.PropagateOptions(strict_corner=False)
+    for _ in range(30):
+        d = int(rng.choice([17, 20, 33, 64, 130]))
+        lx, ly = int(rng.integers(40, 900)), int(rng.integers(40, 900))
+        order = int(rng.choice([4, 8, 12]))
+        x = np.cumsum(rng.normal(0.0, 1.0 / np.sqrt(lx), size=(lx, d)), axis=0)
+        y = np.cumsum(rng.normal(0.0, 1.0 / np.sqrt(ly), size=(ly, d)), axis=0)
+        monkeypatch.delenv("SK_NO_INTRA", raising=False)
+        monkeypatch.delenv("SK_NO_OVERLAP", raising=False)
+        a = sk.propagate(x, y, order, opts).value
+        monkeypatch.setenv("SK_NO_INTRA", "1")
+        monkeypatch.setenv("SK_NO_OVERLAP", "1")
+        b = sk.propagate(x, y, order, opts).value
+        assert np.float64(a).view(np.int64) == np.float64(b).view(np.int64), (d, lx, ly, order)
+
+
 @pytest.mark.parametrize("kernel", ["register", "runtime"])
 def test_literal_kernels_bit_identical_to_the_reference(sk, restatement, monkeypatch, kernel):
     """The literal kernels -- the order-8 register-resident one the strict
